@@ -133,6 +133,8 @@ def _declare(L):
     L.orc_kron_solve.restype = C.c_int
     L.orc_kron_solve.argtypes = [C.c_int, _dp, _dp, _dp]
     L.orc_free.argtypes = [C.c_void_p]
+    L.orc_set_model.argtypes = [C.c_int]
+    L.orc_get_model.restype = C.c_int
 
 
 # ----------------------------------------------------------------- helpers
@@ -160,6 +162,25 @@ def _take(ptr, rows: int, cols: int) -> np.ndarray:
 
 
 # ----------------------------------------------------------------- API
+MODELS = {"chop": 0, "tc": 1}
+
+
+class model:
+    """Context manager selecting the u_s precision model ("chop" or "tc")."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        self.prev = lib().orc_get_model()
+        lib().orc_set_model(MODELS[self.name])
+        return self
+
+    def __exit__(self, *exc):
+        lib().orc_set_model(self.prev)
+        return False
+
+
 def unit_roundoff(p) -> float:
     return lib().orc_unit_roundoff(_prec(p))
 

@@ -116,20 +116,34 @@ static int exponent_of_max(long len, const double *a)
 /* Matrix product at precision p (used for every "A_{k-1}^{-1} Z_{k-1}", */
 /* "A Z_i", "T_i N_i T_i^T", ... of the paper).                          */
 /* ------------------------------------------------------------------ */
+/* Precision model of "computation at precision u_s" for the u_s matrix
+ * operations (products, inversions):
+ *   ORC_MODEL_CHOP (0): every scalar operation rounded to u_s -- the paper's
+ *       chop-based simulation (l.1400-1401);
+ *   ORC_MODEL_TC (1): operands and results stored in u_s, inner products and
+ *       eliminations carried in fp32 -- the tensor-core arithmetic the paper
+ *       targets (fp16 tensor cores with fp32 accumulation, l.67-70).
+ * For u_s in {fp32, fp64} both models coincide.  Reading R-TC. */
+static int g_model = 0;
+void orc_set_model(int model) { g_model = model; }
+int orc_get_model(void) { return g_model; }
+static int acc_prec(int p) { return (g_model == 1 && (p == ORC_FP16 || p == ORC_BF16)) ? ORC_FP32 : p; }
+
 void orc_gemm(int p, int ta, int tb, int m, int n, int k,
               const double *A, int lda, const double *B, int ldb,
               double *C, int ldc)
 {
+    const int q = acc_prec(p);     /* accumulation precision */
     for (int j = 0; j < n; j++)
         for (int i = 0; i < m; i++) {
             double s = 0.0;
             for (int l = 0; l < k; l++) {
                 double a = ta ? A[IDX(l, i, lda)] : A[IDX(i, l, lda)];
                 double b = tb ? B[IDX(j, l, ldb)] : B[IDX(l, j, ldb)];
-                double pr = FL(a * b);
-                s = (l == 0) ? pr : FL(s + pr);
+                double pr = rnd(a * b, q);
+                s = (l == 0) ? pr : rnd(s + pr, q);
             }
-            C[IDX(i, j, ldc)] = s;
+            C[IDX(i, j, ldc)] = rnd(s, p);
         }
 }
 
@@ -170,8 +184,9 @@ int orc_getrf(int p, int n, double *A, int lda, int *piv)
     return 0;
 }
 
-int orc_inverse(int p, int n, const double *A, double *Ainv, int *piv_out)
+int orc_inverse(int pout, int n, const double *A, double *Ainv, int *piv_out)
 {
+    const int p = acc_prec(pout);   /* TC model: eliminations in fp32, result stored in u_s */
     double *LU = dcopy(A, (long)n * n);
     int *piv = (int *)malloc(sizeof(int) * (n > 0 ? n : 1));
     int info = orc_getrf(p, n, LU, n, piv);
@@ -194,7 +209,7 @@ int orc_inverse(int p, int n, const double *A, double *Ainv, int *piv_out)
             if (xl == 0.0) continue;
             for (int i = 0; i < l; i++) y[i] = FL(y[i] - FL(LU[IDX(i, l, n)] * xl));
         }
-        for (int i = 0; i < n; i++) Ainv[IDX(i, j, n)] = y[i];
+        for (int i = 0; i < n; i++) Ainv[IDX(i, j, n)] = rnd(y[i], pout);
     }
     if (piv_out) memcpy(piv_out, piv, sizeof(int) * n);
     free(y); free(LU); free(piv);

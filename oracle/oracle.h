@@ -31,6 +31,11 @@ double orc_round(double x, int prec);      /* fast exact path */
 double orc_round_ref(double x, int prec);  /* the definition */
 void   orc_round_array(double *x, long len, int prec);
 
+/* precision model of u_s matrix operations: 0 = chop (per operation),
+ * 1 = tensor-core (u_s storage, fp32 accumulation); see oracle.c */
+void orc_set_model(int model);
+int  orc_get_model(void);
+
 /* C(m x n) = op(A) op(B), every product and partial sum rounded to prec,
  * inner products accumulated in index order. */
 void orc_gemm(int prec, int ta, int tb, int m, int n, int k,

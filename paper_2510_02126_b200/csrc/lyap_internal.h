@@ -1,0 +1,54 @@
+// lyap_internal.h -- internal interfaces between the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+
+namespace lyap {
+
+// Workspace of the blocked Gauss-Jordan inversion (gje.cu).
+struct GjeWork {
+    int n = 0, prec = 0;
+    void *X = nullptr, *B = nullptr, *tmp = nullptr, *Pglob = nullptr;
+    int *ints = nullptr;
+    int *ipiv = nullptr, *rowperm = nullptr, *invperm = nullptr, *moved = nullptr;
+    int *nmoved = nullptr, *info = nullptr, *tmp_perm = nullptr;
+    int alloc(int n, int prec);
+    void release();
+};
+
+int gje_invert(cudaStream_t s, int n, int prec, void *A, GjeWork &w);
+int col_gather(cudaStream_t s, int n, int prec, const void *G, const int *invperm, void *out);
+template <typename T> int gemm_update(cudaStream_t s, int n, int b, const T *X, const T *B, T *A);
+
+// fp64 dense kernels (qr.cu, eig.cu, rrqr.cu)
+struct QrWork {
+    int mmax = 0, nmax = 0;
+    double *V = nullptr, *T = nullptr, *W = nullptr, *tau = nullptr, *Wk = nullptr;
+    int alloc(int mmax, int nmax);
+    void release();
+};
+// Q (m x k) and R (k x n), k = min(m, n), column-major, diag(R) >= 0.
+int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, QrWork &w);
+
+struct EigWork {
+    int nmax = 0;
+    double *A = nullptr, *V = nullptr, *scal = nullptr;
+    int *ints = nullptr;
+    int alloc(int nmax);
+    void release();
+};
+// w descending, V columns (largest-|component| positive); A is not modified.
+int syev_f64(cudaStream_t s, int n, const double *A, double *w, double *V, EigWork &e);
+
+struct RrqrWork {
+    int nmax = 0, cmax = 0;
+    double *M = nullptr, *nrm = nullptr, *scal = nullptr;
+    int *ints = nullptr;
+    int alloc(int nmax, int cmax);
+    void release();
+};
+// RankTruncChol: returns the kept rank in *k (host), Zout n x k.
+int rank_trunc_chol_f64(cudaStream_t s, int n, int c, const double *Z, double tol, int prec_out,
+                        double *Zout, int *k, RrqrWork &w);
+
+}  // namespace lyap

@@ -1,0 +1,536 @@
+// newton.cu -- element-wise / reduction kernels of the sign-function Newton
+// iteration (Section 3, Eqs. newton-lyapu, newton-lyapu-factored-*)
+// and of the fp64 fragments.
+//
+//  * cast kernel: A (fp64) -> A_0 in the solver precision u_s, with
+//    max|a| and ||A_0||_F (the "norm-scaling and cast" step);
+//  * scale kernel: W = 2^{-e} A_k (exact power-of-two range scaling so that
+//    the inversion stays inside the fp16/bf16 range, reading R-RANGE);
+//  * Newton update kernel (fused): A_{k+1} = (mu A_k + mu^{-1} A_k^{-1})/2
+//    with the column un-permutation of the Gauss-Jordan result, the cached
+//    copy of A_k^{-1}, and per-row partials of ||A_{k+1}-A_k||_F,
+//    ||A_{k+1}||_F, ||A_{k+1}+I||_inf and max|A_{k+1}|;
+//  * Z-side helpers (range scaling of L, blkdiag(mu Y, mu^{-1} Y)/2, the
+//    Cholesky column scalings), selection / gather kernels for truncations.
+#include "common.cuh"
+#include "lyap_internal.h"
+#include "newton_kernels.h"
+
+namespace lyap {
+
+// ------------------------------------------------------------ row partials
+// part[4*i + 0..3] = per-row partial sums, reduced by reduce_rows_kernel in a
+// fixed order (deterministic).
+template <typename T>
+__global__ void __launch_bounds__(256)
+cast_kernel(int n, const double *__restrict__ A, T *__restrict__ Ak, double *__restrict__ part)
+{
+    __shared__ double red[32];
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        double ss = 0.0, mx = 0.0;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+            T v = from_d<T>(A[(long)i * n + j]);
+            Ak[(long)i * n + j] = v;
+            double d = to_d<T>(v);
+            ss = fma(d, d, ss);
+            mx = fmax(mx, fabs(d));
+        }
+        ss = block_sum(ss, red);
+        mx = block_max(mx, red);
+        if (threadIdx.x == 0) { part[4 * i + 0] = 0.0; part[4 * i + 1] = ss; part[4 * i + 2] = 0.0; part[4 * i + 3] = mx; }
+    }
+}
+
+// out[0] = sum part[.,0], out[1] = sum part[.,1], out[2] = max part[.,2], out[3] = max part[.,3]
+__global__ void __launch_bounds__(1024)
+reduce_rows_kernel(int n, const double *__restrict__ part, double *__restrict__ out)
+{
+    __shared__ double red[32];
+    double s0 = 0.0, s1 = 0.0, m2 = 0.0, m3 = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        s0 += part[4 * i]; s1 += part[4 * i + 1];
+        m2 = fmax(m2, part[4 * i + 2]); m3 = fmax(m3, part[4 * i + 3]);
+    }
+    s0 = block_sum(s0, red); s1 = block_sum(s1, red);
+    m2 = block_max(m2, red); m3 = block_max(m3, red);
+    if (threadIdx.x == 0) { out[0] = s0; out[1] = s1; out[2] = m2; out[3] = m3; }
+}
+
+// W = 2^{-e} A_k with e = exponent of max|A_k| (scal[SC_MAXA]) so that max|W| in [0.5,1).
+template <typename T>
+__global__ void scale_kernel(long nn, const T *__restrict__ Ak, T *__restrict__ W, double *__restrict__ scal)
+{
+    int e;
+    frexp(scal[SC_MAXA], &e);
+    if (scal[SC_MAXA] == 0.0) e = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) scal[SC_EXP] = (double)e;
+    const float f = ldexpf(1.0f, -e);
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < nn; idx += (long)gridDim.x * blockDim.x) {
+        if constexpr (sizeof(T) == 8) W[idx] = ldexp(to_d<T>(Ak[idx]), -e);
+        else W[idx] = from_f<T>(to_f<T>(Ak[idx]) * f);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+sumsq_rows_kernel(int n, const T *__restrict__ G, double *__restrict__ part)
+{
+    __shared__ double red[32];
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        double ss = 0.0;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) { double d = to_d<T>(G[(long)i * n + j]); ss = fma(d, d, ss); }
+        ss = block_sum(ss, red);
+        if (threadIdx.x == 0) { part[4 * i] = ss; part[4 * i + 1] = 0.0; part[4 * i + 2] = 0.0; part[4 * i + 3] = 0.0; }
+    }
+}
+
+// mu (Frobenius scaling, l.1139) from ||G||_F^2 (scal[SC_RED+0]), ||A_k||_F^2 (scal[SC_NA2]), e.
+__global__ void mu_kernel(int scaling, double *scal)
+{
+    double e = scal[SC_EXP];
+    double ng = sqrt(scal[SC_RED + 0]);
+    double ninv = ldexp(ng, -(int)e);             // ||A_k^{-1}||_F = 2^{-e} ||G||_F
+    double na = sqrt(scal[SC_NA2]);
+    double mu = 1.0;
+    if (scaling && na > 0.0 && ninv > 0.0 && isfinite(na) && isfinite(ninv)) mu = sqrt(ninv / na);
+    scal[SC_MU] = mu;
+}
+
+// A_{k+1} = 0.5 (mu A_k + mu^{-1} A_k^{-1}),  A_k^{-1}[i][j] = 2^{-e} G[i][invperm[j]].
+template <typename T>
+__global__ void __launch_bounds__(256)
+newton_update_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ G, const int *__restrict__ invperm,
+                     T *__restrict__ Anext, T *__restrict__ Ainv, const double *__restrict__ scal,
+                     double *__restrict__ part)
+{
+    __shared__ double red[32];
+    using Acc = typename Prec<T>::acc;
+    const double mu = scal[SC_MU];
+    const int e = (int)scal[SC_EXP];
+    const Acc a = (Acc)mu, b = (Acc)(1.0 / mu);
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        double dd = 0.0, ss = 0.0, rs = 0.0, mx = 0.0;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+            T gi;
+            if constexpr (sizeof(T) == 8) gi = ldexp(G[(long)i * n + invperm[j]], -e);
+            else gi = from_f<T>(ldexpf(to_f<T>(G[(long)i * n + invperm[j]]), -e));
+            Ainv[(long)i * n + j] = gi;
+            Acc x = to_acc<T>(Ak[(long)i * n + j]);
+            Acc y = to_acc<T>(gi);
+            T nv = from_acc<T>(Acc(0.5) * fma(a, x, b * y));
+            Anext[(long)i * n + j] = nv;
+            double nd = to_d<T>(nv), xd = (double)x;
+            dd = fma(nd - xd, nd - xd, dd);
+            ss = fma(nd, nd, ss);
+            rs += fabs(nd + (i == j ? 1.0 : 0.0));
+            mx = fmax(mx, fabs(nd));
+            if (!isfinite(nd)) mx = INFINITY;
+        }
+        dd = block_sum(dd, red); ss = block_sum(ss, red);
+        rs = block_sum(rs, red); mx = block_max(mx, red);
+        if (threadIdx.x == 0) { part[4 * i] = dd; part[4 * i + 1] = ss; part[4 * i + 2] = rs; part[4 * i + 3] = mx; }
+    }
+}
+
+// ------------------------------------------------------------ Z side
+// Zt (n x m, T) = round(2^{-e} L) with e = exponent of max|L| (computed here, one CTA).
+template <typename T>
+__global__ void __launch_bounds__(1024)
+load_factor_kernel(long len, const double *__restrict__ L, T *__restrict__ Zt, double *__restrict__ scal, int slot)
+{
+    __shared__ double red[32];
+    double mx = 0.0;
+    for (long i = threadIdx.x; i < len; i += blockDim.x) mx = fmax(mx, fabs(L[i]));
+    mx = block_max(mx, red);
+    int e = 0;
+    if (mx > 0.0 && isfinite(mx)) frexp(mx, &e);
+    if (threadIdx.x == 0) scal[slot] = (double)e;
+    for (long i = threadIdx.x; i < len; i += blockDim.x) Zt[i] = from_d<T>(ldexp(L[i], -e));
+}
+
+// Y (m x m fp64) = round_us(2^{-e} S), e = exponent of max|S|; one CTA.
+__global__ void load_inner_kernel(int m, const double *__restrict__ S, double *__restrict__ Y, int ldy,
+                                  int prec, double *__restrict__ scal, int slot)
+{
+    __shared__ double red[32];
+    double mx = 0.0;
+    for (int i = threadIdx.x; i < m * m; i += blockDim.x) mx = fmax(mx, fabs(S[i]));
+    mx = block_max(mx, red);
+    int e = 0;
+    if (mx > 0.0 && isfinite(mx)) frexp(mx, &e);
+    if (threadIdx.x == 0) scal[slot] = (double)e;
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+        int i = idx % m, j = idx / m;
+        Y[i + (long)j * ldy] = round_to(ldexp(S[idx], -e), prec);
+    }
+}
+
+// Ynew (2c x 2c, ld ldn) = blkdiag(round(a Y), round(b Y)) with a = mu/2, b = 1/(2 mu).
+__global__ void y_blkdiag_kernel(int c, const double *__restrict__ Y, int ldy, double *__restrict__ Yn, int ldn,
+                                 double a, double b, int prec)
+{
+    long tot = (long)4 * c * c;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < tot; idx += (long)gridDim.x * blockDim.x) {
+        int i = (int)(idx % (2 * c)), j = (int)(idx / (2 * c));
+        double v = 0.0;
+        if (i < c && j < c) v = round_to(a * Y[i + (long)j * ldy], prec);
+        else if (i >= c && j >= c) v = round_to(b * Y[(i - c) + (long)(j - c) * ldy], prec);
+        Yn[i + (long)j * ldn] = v;
+    }
+}
+
+// Cholesky Z-side: Z[:, 0:c] *= a, Z[:, c:2c] *= b (rounded to T).
+template <typename T>
+__global__ void chol_scale_kernel(long nc, T *__restrict__ Z, float a, float b)
+{
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < 2 * nc; idx += (long)gridDim.x * blockDim.x) {
+        float f = (idx < nc) ? a : b;
+        Z[idx] = from_f<T>(to_f<T>(Z[idx]) * f);
+    }
+}
+template <>
+__global__ void chol_scale_kernel<double>(long nc, double *__restrict__ Z, float a, float b) {}
+
+__global__ void chol_scale_kernel_d(long nc, double *__restrict__ Z, double a, double b)
+{
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < 2 * nc; idx += (long)gridDim.x * blockDim.x)
+        Z[idx] *= (idx < nc) ? a : b;
+}
+
+template <typename T>
+__global__ void to_f64_kernel(long len, const T *__restrict__ x, double *__restrict__ y, double f)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < len; i += (long)gridDim.x * blockDim.x)
+        y[i] = to_d<T>(x[i]) * f;
+}
+template <typename T>
+__global__ void from_f64_kernel(long len, const double *__restrict__ x, T *__restrict__ y)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < len; i += (long)gridDim.x * blockDim.x)
+        y[i] = from_d<T>(x[i]);
+}
+// Z_final = round_T(Z * s1) * 2^{e}  (Cholesky: s1 = 1/sqrt(2); LDL^T: s1 = 1)
+template <typename T>
+__global__ void finish_factor_kernel(long len, const T *__restrict__ x, double *__restrict__ y, double s1,
+                                     const double *__restrict__ scal, int slot)
+{
+    int e = (int)scal[slot];
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < len; i += (long)gridDim.x * blockDim.x) {
+        double v = to_d<T>(x[i]);
+        if (s1 != 1.0) v = to_d<T>(from_d<T>(v * s1));
+        y[i] = ldexp(v, e);
+    }
+}
+
+// ------------------------------------------------------------ selection
+// mode 0: |w| >= thr ; 1: |w| > thr ; 2: w >= thr ; 3: w <= -thr.  thr = rel * max|w|.
+// idx[0..cnt) in order; cnt written to *cnt (device).  One CTA.
+__global__ void __launch_bounds__(1024)
+select_kernel(int k, const double *__restrict__ w, double rel, int mode, int *__restrict__ idx, int *__restrict__ cnt)
+{
+    __shared__ double red[32];
+    __shared__ int wc[32];
+    double mx = 0.0;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) mx = fmax(mx, fabs(w[i]));
+    mx = block_max(mx, red);
+    const double thr = rel * mx;
+    int base = 0;
+    for (int i0 = 0; i0 < k; i0 += blockDim.x) {
+        int i = i0 + threadIdx.x;
+        bool keep = false;
+        if (i < k) {
+            double v = w[i];
+            keep = (mode == 0) ? fabs(v) >= thr : (mode == 1) ? fabs(v) > thr : (mode == 2) ? v >= thr : v <= -thr;
+            if (mx == 0.0) keep = false;
+        }
+        unsigned bal = __ballot_sync(0xffffffffu, keep);
+        int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        if (lane == 0) wc[wid] = __popc(bal);
+        __syncthreads();
+        int off = base;
+        for (int q = 0; q < wid; q++) off += wc[q];
+        if (keep) idx[off + __popc(bal & ((1u << lane) - 1u))] = i;
+        int tot = 0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); q++) tot += wc[q];
+        base += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *cnt = base;
+}
+
+// out[:, t] = V[:, idx[t]] * f(w[idx[t]]) ; fmode 0: 1, 1: sqrt(w), 2: sqrt(-w)
+__global__ void gather_cols_kernel(int rows, int cnt, const double *__restrict__ V, int ldv, const int *__restrict__ idx,
+                                   const double *__restrict__ w, int fmode, double *__restrict__ out, int ldo)
+{
+    long tot = (long)rows * cnt;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        int i = (int)(e % rows), t = (int)(e / rows);
+        int c = idx[t];
+        double f = 1.0;
+        if (fmode == 1) f = sqrt(w[c]);
+        else if (fmode == 2) f = sqrt(-w[c]);
+        out[i + (long)t * ldo] = V[i + (long)c * ldv] * f;
+    }
+}
+
+// Y (cnt x cnt) = diag(round_prec(w[idx[t]])), zero elsewhere.
+__global__ void diag_from_sel_kernel(int cnt, const double *__restrict__ w, const int *__restrict__ idx, int prec,
+                                     double *__restrict__ Y, int ldy)
+{
+    long tot = (long)cnt * cnt;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        int i = (int)(e % cnt), j = (int)(e / cnt);
+        Y[i + (long)j * ldy] = (i == j) ? round_to(w[idx[i]], prec) : 0.0;
+    }
+}
+
+__global__ void round_array_kernel(long len, double *__restrict__ x, int prec)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < len; i += (long)gridDim.x * blockDim.x)
+        x[i] = round_to(x[i], prec);
+}
+
+// copy a (rows x cols, ld lda) block into b (ld ldb), optional scale
+__global__ void copy_block_kernel(int rows, int cols, const double *__restrict__ a, int lda, double *__restrict__ b,
+                                  int ldb, double f)
+{
+    long tot = (long)rows * cols;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        int i = (int)(e % rows), j = (int)(e / rows);
+        b[i + (long)j * ldb] = f * a[i + (long)j * lda];
+    }
+}
+
+__global__ void zero_kernel(long len, double *__restrict__ x)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < len; i += (long)gridDim.x * blockDim.x) x[i] = 0.0;
+}
+
+// N = [0 Y 0; Y 0 0; 0 0 S] (p x p, p = 2c+m) or P (Y = I, S = I) when Y == nullptr.
+__global__ void build_N_kernel(int c, int m, const double *__restrict__ Y, int ldy, const double *__restrict__ S,
+                               double *__restrict__ N)
+{
+    const int p = 2 * c + m;
+    long tot = (long)p * p;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        int i = (int)(e % p), j = (int)(e / p);
+        double v = 0.0;
+        if (i < c && j >= c && j < 2 * c) v = Y ? Y[i + (long)(j - c) * ldy] : (i == j - c ? 1.0 : 0.0);
+        else if (i >= c && i < 2 * c && j < c) v = Y ? Y[(i - c) + (long)j * ldy] : (i - c == j ? 1.0 : 0.0);
+        else if (i >= 2 * c && j >= 2 * c) v = S ? S[(i - 2 * c) + (long)(j - 2 * c) * m] : (i == j ? 1.0 : 0.0);
+        N[e] = v;
+    }
+}
+
+// Ups = blkdiag(Y (c x c), Yd (cd x cd)) or signature J = blkdiag(I_c, I_cp, -I_cm) when Y == nullptr
+__global__ void build_blkdiag_kernel(int c, int cd, const double *__restrict__ Y, int ldy, const double *__restrict__ Yd,
+                                     int ldyd, int cp, double *__restrict__ U)
+{
+    const int p = c + cd;
+    long tot = (long)p * p;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        int i = (int)(e % p), j = (int)(e / p);
+        double v = 0.0;
+        if (Y) {
+            if (i < c && j < c) v = Y[i + (long)j * ldy];
+            else if (i >= c && j >= c) v = Yd[(i - c) + (long)(j - c) * ldyd];
+        } else if (i == j) {
+            v = (i < c + cp) ? 1.0 : -1.0;
+        }
+        U[e] = v;
+    }
+}
+
+// trace(M) for the Frobenius norms of implied products, sum_i sum_j P_ij P_ji
+__global__ void __launch_bounds__(1024)
+trace_prod_kernel(int k, const double *__restrict__ P, double *__restrict__ out)
+{
+    __shared__ double red[32];
+    double s = 0.0;
+    for (long e = threadIdx.x; e < (long)k * k; e += blockDim.x) {
+        int i = (int)(e % k), j = (int)(e / k);
+        s = fma(P[e], P[j + (long)i * k], s);
+    }
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) *out = s;
+}
+
+// ------------------------------------------------------------ launchers
+static inline int grid_for(long n, int bs = 256, int cap = 4096) { int g = ceil_div(n, bs); return g < 1 ? 1 : (g > cap ? cap : g); }
+
+#define DISPATCH_T(prec, F, ...)                                        \
+    switch (prec) {                                                     \
+        case LYAP_FP64: F<double>(__VA_ARGS__); break;                  \
+        case LYAP_FP32: F<float>(__VA_ARGS__); break;                   \
+        case LYAP_FP16: F<__half>(__VA_ARGS__); break;                  \
+        case LYAP_BF16: F<__nv_bfloat16>(__VA_ARGS__); break;           \
+        default: return LYAP_ERR_ARG;                                   \
+    }
+
+template <typename T> static void k_cast(cudaStream_t s, int n, const double *A, void *Ak, double *part)
+{ cast_kernel<T><<<n < 4096 ? n : 4096, 256, 0, s>>>(n, A, (T *)Ak, part); }
+int nk_cast(cudaStream_t s, int prec, int n, const double *A, void *Ak, double *part, double *out)
+{
+    DISPATCH_T(prec, k_cast, s, n, A, Ak, part);
+    LYAP_TRY(launched());
+    reduce_rows_kernel<<<1, 1024, 0, s>>>(n, part, out);
+    return launched();
+}
+
+template <typename T> static void k_scale(cudaStream_t s, long nn, const void *Ak, void *W, double *scal)
+{ scale_kernel<T><<<grid_for(nn), 256, 0, s>>>(nn, (const T *)Ak, (T *)W, scal); }
+int nk_scale(cudaStream_t s, int prec, long nn, const void *Ak, void *W, double *scal)
+{
+    DISPATCH_T(prec, k_scale, s, nn, Ak, W, scal);
+    return launched();
+}
+
+template <typename T> static void k_sumsq(cudaStream_t s, int n, const void *G, double *part)
+{ sumsq_rows_kernel<T><<<n < 4096 ? n : 4096, 256, 0, s>>>(n, (const T *)G, part); }
+int nk_mu(cudaStream_t s, int prec, int n, const void *G, double *part, double *scal, int scaling)
+{
+    DISPATCH_T(prec, k_sumsq, s, n, G, part);
+    LYAP_TRY(launched());
+    reduce_rows_kernel<<<1, 1024, 0, s>>>(n, part, scal + SC_RED);
+    LYAP_TRY(launched());
+    mu_kernel<<<1, 1, 0, s>>>(scaling, scal);
+    return launched();
+}
+
+template <typename T> static void k_update(cudaStream_t s, int n, const void *Ak, const void *G, const int *ip,
+                                           void *An, void *Ai, const double *scal, double *part)
+{ newton_update_kernel<T><<<n < 4096 ? n : 4096, 256, 0, s>>>(n, (const T *)Ak, (const T *)G, ip, (T *)An, (T *)Ai, scal, part); }
+int nk_update(cudaStream_t s, int prec, int n, const void *Ak, const void *G, const int *invperm, void *Anext,
+              void *Ainv, double *scal, double *part)
+{
+    DISPATCH_T(prec, k_update, s, n, Ak, G, invperm, Anext, Ainv, scal, part);
+    LYAP_TRY(launched());
+    reduce_rows_kernel<<<1, 1024, 0, s>>>(n, part, scal + SC_RED);
+    return launched();
+}
+
+template <typename T> static void k_loadf(cudaStream_t s, long len, const double *L, void *Zt, double *scal, int slot)
+{ load_factor_kernel<T><<<1, 1024, 0, s>>>(len, L, (T *)Zt, scal, slot); }
+int nk_load_factor(cudaStream_t s, int prec, long len, const double *L, void *Zt, double *scal, int slot)
+{
+    DISPATCH_T(prec, k_loadf, s, len, L, Zt, scal, slot);
+    return launched();
+}
+int nk_load_inner(cudaStream_t s, int prec, int m, const double *S, double *Y, int ldy, double *scal, int slot)
+{
+    load_inner_kernel<<<1, 256, 0, s>>>(m, S, Y, ldy, prec, scal, slot);
+    return launched();
+}
+int nk_y_blkdiag(cudaStream_t s, int c, const double *Y, int ldy, double *Yn, int ldn, double a, double b, int prec)
+{
+    y_blkdiag_kernel<<<grid_for(4L * c * c), 256, 0, s>>>(c, Y, ldy, Yn, ldn, a, b, prec);
+    return launched();
+}
+template <typename T> static void k_cs(cudaStream_t s, long nc, void *Z, double a, double b)
+{
+    if constexpr (sizeof(T) == 8) chol_scale_kernel_d<<<grid_for(2 * nc), 256, 0, s>>>(nc, (double *)Z, a, b);
+    else chol_scale_kernel<T><<<grid_for(2 * nc), 256, 0, s>>>(nc, (T *)Z, (float)a, (float)b);
+}
+int nk_chol_scale(cudaStream_t s, int prec, long nc, void *Z, double a, double b)
+{
+    DISPATCH_T(prec, k_cs, s, nc, Z, a, b);
+    return launched();
+}
+template <typename T> static void k_tof64(cudaStream_t s, long len, const void *x, double *y, double f)
+{ to_f64_kernel<T><<<grid_for(len), 256, 0, s>>>(len, (const T *)x, y, f); }
+int nk_to_f64(cudaStream_t s, int prec, long len, const void *x, double *y, double f)
+{
+    DISPATCH_T(prec, k_tof64, s, len, x, y, f);
+    return launched();
+}
+template <typename T> static void k_fromf64(cudaStream_t s, long len, const double *x, void *y)
+{ from_f64_kernel<T><<<grid_for(len), 256, 0, s>>>(len, x, (T *)y); }
+int nk_from_f64(cudaStream_t s, int prec, long len, const double *x, void *y)
+{
+    DISPATCH_T(prec, k_fromf64, s, len, x, y);
+    return launched();
+}
+template <typename T> static void k_finish(cudaStream_t s, long len, const void *x, double *y, double s1, const double *scal, int slot)
+{ finish_factor_kernel<T><<<grid_for(len), 256, 0, s>>>(len, (const T *)x, y, s1, scal, slot); }
+int nk_finish_factor(cudaStream_t s, int prec, long len, const void *x, double *y, double s1, const double *scal, int slot)
+{
+    DISPATCH_T(prec, k_finish, s, len, x, y, s1, scal, slot);
+    return launched();
+}
+int nk_select(cudaStream_t s, int k, const double *w, double rel, int mode, int *idx, int *cnt)
+{
+    select_kernel<<<1, 1024, 0, s>>>(k, w, rel, mode, idx, cnt);
+    return launched();
+}
+int nk_gather_cols(cudaStream_t s, int rows, int cnt, const double *V, int ldv, const int *idx, const double *w,
+                   int fmode, double *out, int ldo)
+{
+    if (rows <= 0 || cnt <= 0) return LYAP_OK;
+    gather_cols_kernel<<<grid_for((long)rows * cnt), 256, 0, s>>>(rows, cnt, V, ldv, idx, w, fmode, out, ldo);
+    return launched();
+}
+int nk_diag_from_sel(cudaStream_t s, int cnt, const double *w, const int *idx, int prec, double *Y, int ldy)
+{
+    if (cnt <= 0) return LYAP_OK;
+    diag_from_sel_kernel<<<grid_for((long)cnt * cnt), 256, 0, s>>>(cnt, w, idx, prec, Y, ldy);
+    return launched();
+}
+int nk_round(cudaStream_t s, long len, double *x, int prec)
+{
+    if (prec == LYAP_FP64 || len <= 0) return LYAP_OK;
+    round_array_kernel<<<grid_for(len), 256, 0, s>>>(len, x, prec);
+    return launched();
+}
+int nk_copy_block(cudaStream_t s, int rows, int cols, const double *a, int lda, double *b, int ldb, double f)
+{
+    if (rows <= 0 || cols <= 0) return LYAP_OK;
+    copy_block_kernel<<<grid_for((long)rows * cols), 256, 0, s>>>(rows, cols, a, lda, b, ldb, f);
+    return launched();
+}
+int nk_zero(cudaStream_t s, long len, double *x)
+{
+    if (len <= 0) return LYAP_OK;
+    zero_kernel<<<grid_for(len), 256, 0, s>>>(len, x);
+    return launched();
+}
+int nk_build_N(cudaStream_t s, int c, int m, const double *Y, int ldy, const double *S, double *N)
+{
+    long p = 2L * c + m;
+    build_N_kernel<<<grid_for(p * p), 256, 0, s>>>(c, m, Y, ldy, S, N);
+    return launched();
+}
+int nk_build_blkdiag(cudaStream_t s, int c, int cd, const double *Y, int ldy, const double *Yd, int ldyd, int cp, double *U)
+{
+    long p = (long)c + cd;
+    build_blkdiag_kernel<<<grid_for(p * p), 256, 0, s>>>(c, cd, Y, ldy, Yd, ldyd, cp, U);
+    return launched();
+}
+__global__ void __launch_bounds__(1024)
+sumsq_vec_kernel(long len, const double *__restrict__ x, double *__restrict__ out)
+{
+    __shared__ double red[32];
+    double s = 0.0;
+    for (long i = threadIdx.x; i < len; i += blockDim.x) s = fma(x[i], x[i], s);
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) *out = s;
+}
+int nk_sumsq(cudaStream_t s, long len, const double *x, double *out)
+{
+    sumsq_vec_kernel<<<1, 1024, 0, s>>>(len, x, out);
+    return launched();
+}
+
+__global__ void roll_kernel(double *scal) { scal[SC_NA2] = scal[SC_RED + 1]; scal[SC_MAXA] = scal[SC_RED + 3]; }
+int nk_roll(cudaStream_t s, double *scal)
+{
+    roll_kernel<<<1, 1, 0, s>>>(scal);
+    return launched();
+}
+
+int nk_trace_prod(cudaStream_t s, int k, const double *P, double *out)
+{
+    trace_prod_kernel<<<1, 1024, 0, s>>>(k, P, out);
+    return launched();
+}
+
+}  // namespace lyap
