@@ -1,0 +1,349 @@
+#!/usr/bin/env python3
+"""bench.py -- time-to-solution of the B200 mixed-precision IR Lyapunov solver.
+
+Contract:
+  python bench.py --gpus N --steps K --warmup W [--impl reference] [--config cfg1]
+
+A "step" is one complete IR solve (Algorithm 2 with the LDL^T
+sign-function Newton solver, Algorithm 4) of BASELINE.json configs[1]:
+n = 1024, m = 4, W = L S L^T, bf16 solver, fp64 refinement, tol 1e-14 -- with
+the inputs resident in HBM.  L2 is flushed (256 MB write) before every timed
+step; step times are CUDA-event device times on the solver's stream.  With N
+ranks every rank solves its own equation (seed 1 + rank; "weak" scaling, no
+data-path collective; the final residual norms are all-gathered over NCCL
+after the timed region).  `value` = solves/s of the whole job.
+
+--impl reference times the CPU oracle (oracle/, plain C) as it stands on the
+host cores: each step is one emulated-bf16 inversion of A_0 (a bounded sample
+of the workload), scaled to solves/s by the number of inversions the method
+needs for this equation.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Lyapunov IR time-to-solution; sign-Newton TFLOP/s as fraction of B200 fp16 peak"
+UNIT = "solves/s"
+
+WORKLOADS = {
+    "cfg0": dict(gen="cfg0", us="fp16", tol=1e-14, maxit=10, max_cols=128,
+                 desc="configs[0]: n=64 m=2 Cholesky W=LL^T, A=Q diag(-lambda) Q^T, fp16 solver, tol 1e-14"),
+    "cfg1": dict(gen="cfg1", us="bf16", tol=1e-14, maxit=50, max_cols=256,
+                 desc="configs[1]: n=1024 m=4 LDL^T W=LSL^T, A=-(Q diag(lambda) Q^T)+K, bf16 solver, "
+                      "fp64 refinement, tol 1e-14"),
+    "cfg2": dict(gen="cfg2", us="fp16", tol=1e-14, maxit=50, max_cols=512,
+                 desc="configs[2]: n=4096 m=8 convection-diffusion 64x64, fp16 solver"),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                    src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------ reference arm (oracle)
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+    import oracle
+    import problems as P
+    wl = WORKLOADS[args.config]
+    p = getattr(P, wl["gen"])()
+    A = p.A
+    oracle.lib()
+    # warm-up: the full A-side sequence gives the number of inversions per solve
+    t0 = time.perf_counter()
+    q = oracle.aseq(wl["us"], A)
+    k_inv = q.steps
+    t_aseq = time.perf_counter() - t0
+    for _ in range(max(0, args.warmup - 1)):
+        oracle.inverse(wl["us"], oracle.round_(A, wl["us"]))
+    times = []
+    Ar = oracle.round_(A, wl["us"])
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.inverse(wl["us"], Ar)
+        times.append(time.perf_counter() - t0)
+    t_inv = sum(times) / len(times)
+    t_solve = t_inv * k_inv
+    value = 1.0 / t_solve
+    sample = (f"one oracle inversion of A_0 per step (emulated {wl['us']}, chop model, n={p.n}); "
+              f"solve time = t_inv x {k_inv} inversions (the A-sequence length; the full A-sequence "
+              f"took {t_aseq:.1f} s); excludes Z-side and refinement work, so CPU throughput is overestimated")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_solve,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": wl["us"],
+            "data": "synthetic", "config": {"workload": wl["desc"], "n": p.n, "m": p.m},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_sample(wl, p, budget_s=30.0):
+    """Oracle as it stands on a bounded sample: the emulated A-side Newton sequence of the same
+    equation (k inversions), single-threaded C."""
+    import oracle
+    t0 = time.perf_counter()
+    q = oracle.aseq(wl["us"], p.A)
+    t = time.perf_counter() - t0
+    return {"value": 1.0 / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle sign-Newton A-sequence ({q.steps} emulated {wl['us']} inversions, chop model) "
+                      f"of the same n={p.n} equation, {t:.1f} s on 1 core; value = 1/that time (excludes the "
+                      f"Z-side and refinement work, i.e. an upper bound on oracle solves/s)"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gpu(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    importlib_build()
+    import paper_2510_02126_b200 as G
+    import problems as P
+    wl = WORKLOADS[args.config]
+    p = getattr(P, wl["gen"])(seed={"cfg0": 0, "cfg1": 1, "cfg2": 2}[args.config] + rank)
+    n, m = p.n, p.m
+    ldlt = p.S is not None
+    A = torch.tensor(p.A, dtype=torch.float64, device=dev)
+    Lt = torch.tensor(np.ascontiguousarray(p.L.T), dtype=torch.float64, device=dev)
+    S = torch.tensor(p.S, dtype=torch.float64, device=dev) if ldlt else None
+    solver = G.Solver(n, us=wl["us"], max_cols=wl["max_cols"])
+    cm = wl["max_cols"]
+    Zt = torch.empty((cm, n), dtype=torch.float64, device=dev)
+    Yb = torch.zeros((cm, cm), dtype=torch.float64, device=dev) if ldlt else None
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)    # 256 MB > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def solve():
+        return solver.solve(A, Lt, S, tol=wl["tol"], maxit=wl["maxit"], out=(Zt, Yb))
+
+    for _ in range(args.warmup):
+        res = solve()
+    # pick the dominant kernel class by device time over one (untimed) solve
+    shares = {}
+    for name in ["gje_update", "gje_panel", "zside_gemm", "jacobi", "qr", "resid_gemm"]:
+        G.kernel_timing(name)
+        solve()
+        ms, cnt = G.kernel_stats()
+        shares[name] = (ms, cnt)
+    G.kernel_timing(None)
+    dom = max(shares, key=lambda k: shares[k][0])
+    # ---- timed region (device time per solve, L2 flushed before each)
+    G.kernel_timing(dom)
+    launches0 = G.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    reports = []
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+            res = solve()
+            ev[i][1].record(stream)
+            reports.append(res.report)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = G.launch_count() - launches0
+    dom_ms, dom_cnt = G.kernel_stats()
+    G.kernel_timing(None)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_max = t.item()
+    value = world * args.steps / (total_max / 1e3)
+    rep = reports[-1]
+    # ---- end-to-end through the host-buffer API (H2D of inputs, D2H of the factors)
+    A_h = torch.tensor(p.A).pin_memory().numpy()
+    L_h = torch.tensor(np.ascontiguousarray(p.L.T)).pin_memory().numpy()
+    S_h = torch.tensor(p.S).pin_memory().numpy() if ldlt else None
+    solver.solve_host(A_h, L_h, S_h, tol=wl["tol"], maxit=wl["maxit"])
+    torch.cuda.synchronize()
+    e2e_t = []
+    rank_h = 0
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        Zh, Yh, rh = solver.solve_host(A_h, L_h, S_h, tol=wl["tol"], maxit=wl["maxit"])
+        e2e_t.append(time.perf_counter() - t0)
+        rank_h = rh["rank"]
+    te = torch.tensor([sum(e2e_t)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * args.steps / te.item()
+    h2d = 8 * (n * n + n * m + (m * m if ldlt else 0))
+    d2h = 8 * (n * rank_h + (cm * rank_h if ldlt else 0))
+    # ---- NCCL gather of the final residual norms (not in the timed data path)
+    resid = torch.tensor([rep["final_res"]], dtype=torch.float64, device=dev)
+    all_res = [resid.clone() for _ in range(world)]
+    if world > 1:
+        dist.all_gather(all_res, resid)
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    pk = load_peaks()
+    # roofline of the dominant kernel class
+    b = 16 if wl["us"] == "fp64" else 32
+    if dom == "gje_update":
+        per_launch = 2.0 * n * n * b                          # rank-b update of all n x n entries
+        bound, unit, peak = "tensor", "TFLOP/s", pk["bf16_sus"]
+        achieved = per_launch / (dom_ms / max(dom_cnt, 1) / 1e3) / 1e12
+    elif dom == "zside_gemm":
+        per_launch = 2.0 * n * n * 2                           # bytes: read one n x n u_s inverse
+        bound, unit, peak = "hbm", "GB/s", pk["hbm"]
+        achieved = per_launch / (dom_ms / max(dom_cnt, 1) / 1e3) / 1e9
+    else:
+        per_launch = None
+        bound, unit, peak, achieved = "latency", "ms/launch", None, dom_ms / max(dom_cnt, 1)
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get(dom)
+    newton_tflops = rep["newton_flops"] / (rep["newton_ms"] / 1e3) / 1e12 if rep["newton_ms"] > 0 else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": wl["us"], "data": "synthetic",
+        "config": {"workload": wl["desc"], "n": n, "m": m, "solver_precision": wl["us"],
+                   "refinement_precision": "fp64", "tol": wl["tol"], "equations_per_gpu": 1,
+                   "l2": "flushed (256 MB write) before every timed step", "parallelism": f"dp{world}"},
+        "time_to_solution_ms": total_max / args.steps,
+        "ir_steps": rep["steps"], "newton_steps_per_call": rep["newton_steps"],
+        "inversions": rep["inversions"], "final_rel_residual": rep["final_res"], "rank": rep["rank"],
+        "status": rep["status"],
+        "phase_ms": {"newton": rep["newton_ms"], "residual": rep["residual_ms"], "update": rep["update_ms"]},
+        "sign_newton_tflops": newton_tflops,
+        "sign_newton_frac_of_fp16_peak": (newton_tflops / pk["bf16"]) if newton_tflops else None,
+        "kernel_class_ms_one_solve": {k: round(v[0], 4) for k, v in shares.items()},
+        "roofline": {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                     "frac": (achieved / peak) if peak else None, "traffic": traffic,
+                     "algorithmic_per_launch": per_launch, "launches_timed": dom_cnt,
+                     "peak_source": pk["src"] + (" sustained" if bound == "tensor" else "")},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "residuals_all_ranks": [r.item() for r in all_res],
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample(wl, p)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def importlib_build():
+    import importlib
+    b = importlib.import_module("paper_2510_02126_b200.build")
+    b.build()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg1", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl != "reference":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

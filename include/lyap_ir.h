@@ -188,6 +188,16 @@ int lyap_sol_upt_chol(lyap_ir_handle h, int c, const double *Z, int cp,
  * reports as gpu_launches). */
 int64_t lyap_launch_count(void);
 
+/* Kernel-class timing for the roofline report: after lyap_kernel_timing(cls)
+ * every launch of class cls (0 Gauss-Jordan rank-b update GEMM, 1 pivoted
+ * panel, 2 A_k^{-1} Z products, 3 Jacobi eigensolver, 4 Householder QR,
+ * 5 fp64 A Z, 6 Newton update; -1 disables) is bracketed by CUDA events on its
+ * launch stream.  lyap_kernel_stats synchronises and returns the summed
+ * device milliseconds and the number of timed launches since the last
+ * lyap_kernel_timing call. */
+int lyap_kernel_timing(int cls);
+int lyap_kernel_stats(double *ms, int64_t *launches);
+
 #ifdef __cplusplus
 }
 #endif

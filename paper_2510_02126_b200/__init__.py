@@ -62,7 +62,10 @@ SYMBOLS = ["lyap_ir_default_options", "lyap_ir_create", "lyap_ir_destroy", "lyap
            "lyap_ir_solve_host", "lyap_invert", "lyap_newton_aseq", "lyap_newton_get_inverse",
            "lyap_newton_z", "lyap_qr", "lyap_syev", "lyap_rank_trunc_chol", "lyap_rank_trunc_ldlt",
            "lyap_res_fac_ldlt", "lyap_res_fac_chol", "lyap_sol_upt_ldlt", "lyap_sol_upt_chol",
-           "lyap_launch_count"]
+           "lyap_launch_count", "lyap_kernel_timing", "lyap_kernel_stats"]
+
+KERNEL_CLASSES = {"gje_update": 0, "gje_panel": 1, "zside_gemm": 2, "jacobi": 3, "qr": 4,
+                  "resid_gemm": 5, "newton_update": 6}
 
 
 def library_path() -> str:
@@ -101,6 +104,8 @@ def lib():
         L.lyap_sol_upt_ldlt.argtypes = [vp, C.c_int, dp, dp, C.c_int, dp, dp, C.c_double, dp, dp, ip]
         L.lyap_sol_upt_chol.argtypes = [vp, C.c_int, dp, C.c_int, dp, C.c_int, dp, C.c_double, dp, ip]
         L.lyap_launch_count.restype = C.c_int64
+        L.lyap_kernel_timing.argtypes = [C.c_int]
+        L.lyap_kernel_stats.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         for s in SYMBOLS:
             if s not in ("lyap_ir_default_options", "lyap_launch_count"):
                 getattr(L, s).restype = C.c_int
@@ -132,6 +137,18 @@ def _stream():
 
 def launch_count() -> int:
     return int(lib().lyap_launch_count())
+
+
+def kernel_timing(cls):
+    """Start timing one kernel class (name or id; None disables)."""
+    c = -1 if cls is None else (KERNEL_CLASSES[cls] if isinstance(cls, str) else int(cls))
+    lib().lyap_kernel_timing(c)
+
+
+def kernel_stats():
+    ms, n = C.c_double(0), C.c_int64(0)
+    lib().lyap_kernel_stats(C.byref(ms), C.byref(n))
+    return ms.value, n.value
 
 
 def default_options(**kw) -> Options:

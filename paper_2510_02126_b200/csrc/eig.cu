@@ -13,6 +13,7 @@
 // eigenvectors up to the sign normalisation applied at the end.
 #include "common.cuh"
 #include "lyap_internal.h"
+#include "ktimer.h"
 
 namespace lyap {
 
@@ -173,7 +174,10 @@ int syev_f64(cudaStream_t s, int n, const double *Ain, double *w, double *Vout, 
     if (n > e.nmax) return LYAP_ERR_CAPACITY;
     LYAP_CUDA_TRY(cudaMemcpyAsync(e.A, Ain, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, s));
     // cs uses scal[8 ...], partner uses ints
-    jacobi_kernel<<<1, 1024, 0, s>>>(n, e.A, e.V, e.scal + 8, e.ints, e.scal);
+    {
+        KTimer kt(KC_JACOBI, s);
+        jacobi_kernel<<<1, 1024, 0, s>>>(n, e.A, e.V, e.scal + 8, e.ints, e.scal);
+    }
     LYAP_TRY(launched());
     int blocks = ceil_div((long)n * 32, 256);
     eig_sort_kernel<<<blocks < 512 ? blocks : 512, 256, 0, s>>>(n, e.A, e.V, w, Vout);

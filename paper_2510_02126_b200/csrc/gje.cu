@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "lyap_internal.h"
+#include "ktimer.h"
 
 namespace lyap {
 
@@ -288,8 +289,11 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
             LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
             attr_set = true;
         }
-        gje_panel_kernel<T><<<1, 1024, sm, s>>>(n, k, b, A, (T *)w.X, w.ipiv + 0, w.moved, w.nmoved,
-                                                w.info, (Acc *)w.Pglob, use_smem ? 1 : 0);
+        {
+            KTimer kt(KC_GJE_PANEL, s);
+            gje_panel_kernel<T><<<1, 1024, sm, s>>>(n, k, b, A, (T *)w.X, w.ipiv + 0, w.moved, w.nmoved,
+                                                    w.info, (Acc *)w.Pglob, use_smem ? 1 : 0);
+        }
         LYAP_TRY(launched());
         dim3 gg(ceil_div(n, 256) < 8 ? ceil_div(n, 256) : 8, 2 * b);
         gje_gather_kernel<T><<<gg, 256, 0, s>>>(n, k, A, w.moved, w.nmoved, (T *)w.tmp, w.rowperm, w.tmp_perm);
@@ -298,7 +302,10 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
         gje_prep_kernel<T><<<gp, 256, 0, s>>>(n, k, b, A, w.moved, w.nmoved, (const T *)w.tmp, w.tmp_perm,
                                               w.rowperm, (T *)w.B);
         LYAP_TRY(launched());
-        LYAP_TRY(gemm_update(s, n, b, (const T *)w.X, (const T *)w.B, A));
+        {
+            KTimer kt(KC_GJE_UPDATE, s);
+            LYAP_TRY(gemm_update(s, n, b, (const T *)w.X, (const T *)w.B, A));
+        }
     }
     invperm_kernel<<<ceil_div(n, 256), 256, 0, s>>>(n, w.rowperm, w.invperm);
     return launched();

@@ -20,6 +20,7 @@
 #include "gemm_simt.cuh"
 #include "lyap_internal.h"
 #include "newton_kernels.h"
+#include "ktimer.h"
 
 namespace lyap { std::atomic<int64_t> g_launches{0}; }
 
@@ -64,6 +65,17 @@ struct lyap_ir_ctx {
 };
 
 namespace {
+
+bool verbose() {
+    static int v = -1;
+    if (v < 0) { const char *e = getenv("LYAP_VERBOSE"); v = (e && e[0] == '1') ? 1 : 0; }
+    return v == 1;
+}
+
+int cap_fail(int line, long need, long have) {
+    fprintf(stderr, "lyap: capacity exceeded at ir.cu:%d (need %ld, have %ld); raise max_cols\n", line, need, have);
+    return LYAP_ERR_CAPACITY;
+}
 
 int dmalloc(void **p, size_t bytes) {
     if (cudaMalloc(p, bytes > 0 ? bytes : 16) != cudaSuccess) return LYAP_ERR_CUDA;
@@ -199,9 +211,12 @@ int zside(lyap_ir_ctx *h, bool ldlt, const double *L, int m, const double *S, do
     const double rho_n = h->opt.rho * n;
     const char *Zbytes = (const char *)h->Zt;
     for (int j = 0; j < h->ksteps; j++) {
-        if (2 * c > h->PZ) return LYAP_ERR_CAPACITY;
+        if (2 * c > h->PZ) return cap_fail(__LINE__, 2 * c, h->PZ);
         const double mu = h->mu[j];
-        LYAP_TRY(zside_gemm(h, h->inv[j], h->Zt, (void *)(Zbytes + h->es * (size_t)n * c), c));
+        {
+            KTimer kt(KC_ZSIDE_GEMM, s);
+            LYAP_TRY(zside_gemm(h, h->inv[j], h->Zt, (void *)(Zbytes + h->es * (size_t)n * c), c));
+        }
         if (ldlt) {
             LYAP_TRY(nk_y_blkdiag(s, c, h->Yc, h->PZ, h->Yn, h->PZ, mu / 2.0, 1.0 / (2.0 * mu), us));
             std::swap(h->Yc, h->Yn);
@@ -213,6 +228,7 @@ int zside(lyap_ir_ctx *h, bool ldlt, const double *L, int m, const double *S, do
             int r = 0;
             if (ldlt) LYAP_TRY(trunc_ldlt(h, c, &r));
             else LYAP_TRY(trunc_chol(h, c, &r));
+            if (verbose()) fprintf(stderr, "lyap:   newton step %d: truncate %d -> %d\n", j, c, r);
             c = r;
         }
     }
@@ -232,8 +248,11 @@ int build_F(lyap_ir_ctx *h, const double *A, const double *L, int m, int c, cons
     const int n = h->n;
     cudaStream_t s = h->s;
     LYAP_TRY(nk_copy_block(s, n, c, Z, n, h->F, n, 1.0));
-    LYAP_TRY(gemm_strided<double, double, double, double>(s, n, c, n, 1.0, A, n, 1, Z, 1, n, 0.0,
-                                                          h->F + (size_t)n * c, 1, n));
+    {
+        KTimer kt(KC_RESID_GEMM, s);
+        LYAP_TRY(gemm_strided<double, double, double, double>(s, n, c, n, 1.0, A, n, 1, Z, 1, n, 0.0,
+                                                              h->F + (size_t)n * c, 1, n));
+    }
     LYAP_TRY(nk_copy_block(s, n, m, L, n, h->F + (size_t)n * 2 * c, n, 1.0));
     return LYAP_OK;
 }
@@ -246,7 +265,7 @@ int res_fac(lyap_ir_ctx *h, const double *A, const double *L, int m, const doubl
     const int n = h->n;
     cudaStream_t s = h->s;
     const int p = 2 * c + m;
-    if (p > h->PW) return LYAP_ERR_CAPACITY;
+    if (p > h->PW) return cap_fail(__LINE__, p, h->PW);
     const int k = std::min(n, p);
     LYAP_TRY(build_F(h, A, L, m, c, Z));
     LYAP_TRY(qr_f64(s, n, p, h->F, h->U, h->Tm, h->qr));
@@ -291,7 +310,7 @@ int sol_upt(lyap_ir_ctx *h, int c, const double *Z, const double *Y, int ldy, in
     const int n = h->n;
     cudaStream_t s = h->s;
     const int p = c + cd + cm;
-    if (p > h->PW) return LYAP_ERR_CAPACITY;
+    if (p > h->PW) return cap_fail(__LINE__, p, h->PW);
     const int k = std::min(n, p);
     LYAP_TRY(nk_copy_block(s, n, c, Z, n, h->F, n, 1.0));
     LYAP_TRY(nk_copy_block(s, n, cd, Zd, n, h->F + (size_t)n * c, n, 1.0));
@@ -428,14 +447,17 @@ int ir_solve(lyap_ir_ctx *h, const double *A, const double *L, int m, const doub
         LYAP_CUDA_TRY(cudaEventSynchronize(h->ev[6]));
         tn += elapsed(h->ev[4], h->ev[5]);
         tu += elapsed(h->ev[5], h->ev[6]);
-        if (2 * cn + m > h->PW) return LYAP_ERR_CAPACITY;
+        if (2 * cn + m > h->PW) return cap_fail(__LINE__, 2 * cn + m, h->PW);
         cur = nxt;
         c = cn;
         R.steps = i;
+        if (verbose())
+            fprintf(stderr, "lyap: step %d rel=%.3e c=%d r=%d rm=%d cd=%d cm=%d -> %d\n", i, rel, c, r, rmm, cd,
+                    cm, cn);
     }
     LYAP_CUDA_TRY(cudaEventRecord(h->ev[7], s));
     LYAP_CUDA_TRY(cudaEventSynchronize(h->ev[7]));
-    if (c > h->cmax) return LYAP_ERR_CAPACITY;
+    if (c > h->cmax) return cap_fail(__LINE__, c, h->cmax);
     LYAP_CUDA_TRY(cudaMemcpyAsync(Zout, h->Zsol[cur], sizeof(double) * (size_t)n * c, cudaMemcpyDeviceToDevice, s));
     if (ldlt && Yout) LYAP_TRY(nk_copy_block(s, c, c, h->Ysol[cur], h->PW, Yout, h->cmax, 1.0));
     LYAP_CUDA_TRY(cudaStreamSynchronize(s));
