@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <atomic>
+#include <algorithm>
 #include "../../include/lyap_ir.h"
 
 namespace lyap {

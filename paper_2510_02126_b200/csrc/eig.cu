@@ -17,6 +17,13 @@
 
 namespace lyap {
 
+// LYAP_EIG=jacobi forces the one-CTA Jacobi at every size (cross-checking).
+static bool force_jacobi() {
+    static int v = -1;
+    if (v < 0) { const char *e = getenv("LYAP_EIG"); v = (e && e[0] == 'j') ? 1 : 0; }
+    return v == 1;
+}
+
 __device__ __forceinline__ void rr_pair(int r, int i, int N, int &a, int &b) {
     if (i == 0) { a = r; b = N - 1; }
     else { a = (r + i) % (N - 1); b = (r - i + (N - 1)) % (N - 1); }
@@ -164,14 +171,23 @@ int EigWork::alloc(int nmax_) {
     LYAP_CUDA_TRY(cudaMalloc(&V, sizeof(double) * (size_t)nmax * nmax));
     LYAP_CUDA_TRY(cudaMalloc(&scal, sizeof(double) * (size_t)(2 * nmax + 16)));
     LYAP_CUDA_TRY(cudaMalloc(&ints, sizeof(int) * (size_t)(nmax + 8)));
+    if (nmax > kJacobiMax) LYAP_TRY(sd.alloc(nmax));
     return LYAP_OK;
 }
-void EigWork::release() { cudaFree(A); cudaFree(V); cudaFree(scal); cudaFree(ints); A = V = scal = nullptr; ints = nullptr; }
+void EigWork::release() {
+    cudaFree(A); cudaFree(V); cudaFree(scal); cudaFree(ints);
+    A = V = scal = nullptr; ints = nullptr;
+    if (sd.pmax) sd.release();
+}
 
 int syev_f64(cudaStream_t s, int n, const double *Ain, double *w, double *Vout, EigWork &e)
 {
     if (n <= 0) return LYAP_OK;
     if (n > e.nmax) return LYAP_ERR_CAPACITY;
+    if (n > kJacobiMax && !force_jacobi()) {
+        KTimer kt(KC_JACOBI, s);
+        return syevd_f64(s, n, Ain, w, Vout, e.sd);
+    }
     LYAP_CUDA_TRY(cudaMemcpyAsync(e.A, Ain, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, s));
     // cs uses scal[8 ...], partner uses ints
     {

@@ -30,13 +30,27 @@ struct QrWork {
 // Q (m x k) and R (k x n), k = min(m, n), column-major, diag(R) >= 0.
 int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, QrWork &w);
 
+// Tridiagonalisation + divide-and-conquer eigensolver (syevd.cu)
+struct SyevdWork {
+    int pmax = 0;
+    double *A = nullptr, *Q = nullptr, *Qg = nullptr, *Qk = nullptr, *U = nullptr, *Qn = nullptr, *R = nullptr;
+    double *vec = nullptr, *rot = nullptr;
+    int *ivec = nullptr;
+    int alloc(int pmax);
+    void release();
+};
+int syevd_f64(cudaStream_t s, int p, const double *A, double *w, double *V, SyevdWork &W);
+
 struct EigWork {
     int nmax = 0;
     double *A = nullptr, *V = nullptr, *scal = nullptr;
     int *ints = nullptr;
+    SyevdWork sd;
     int alloc(int nmax);
     void release();
 };
+// sizes above this use syevd_f64, below the one-CTA Jacobi
+constexpr int kJacobiMax = 32;
 // w descending, V columns (largest-|component| positive); A is not modified.
 int syev_f64(cudaStream_t s, int n, const double *A, double *w, double *V, EigWork &e);
 

@@ -1,0 +1,745 @@
+// syevd.cu -- fp64 symmetric eigensolver for the kernel matrices of Fragments
+// 1-4 and RankTruncLdlt when they are large (ranks of several hundred make
+// H_i, K_i and R Y R^T ~1000 x 1000, PAPER.md l.165, l.240, l.790, l.824,
+// l.1298).  Any backward-stable eigensolver computes "the spectral
+// decomposition" the paper asks for; this one is built for the GPU:
+//
+//  1. Householder tridiagonalisation Q_H^T A Q_H = T in ONE cooperative
+//     kernel: every CTA derives the reflector redundantly from column j, the
+//     symmetric product p = tau A v is column-distributed, a grid barrier,
+//     then the rank-2 update A -= v w^T + w v^T (2 grid barriers per column).
+//  2. Cuppen divide and conquer on T with Gu-Eisenstat eigenvectors:
+//     leaves (<= 32) by warp Jacobi; each merge D + rho z z^T is deflated
+//     (LAPACK dlaed2 rules: rho|z_i| <= tol, close poles rotated together),
+//     the secular roots are found by safeguarded bisection around the nearer
+//     pole (tau stored relative to it), z is recomputed from the roots
+//     (Loewner), and the eigenvector block is a GEMM Q U.
+//  3. Back-transformation X = Q_H Q_T with compact-WY panels (GEMMs).
+#include <cooperative_groups.h>
+#include <algorithm>
+#include <vector>
+#include <cmath>
+#include "common.cuh"
+#include "gemm_simt.cuh"
+#include "lyap_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace lyap {
+
+// ---------------------------------------------------------------- 1. tridiagonalisation
+struct TridArgs {
+    int p;
+    double *A;      // p x p col-major (symmetric), trailing block updated in place
+    double *R;      // p x p col-major: reflector j in R[j+1:p, j] (R[j+1, j] = 1)
+    double *d, *e, *tau;
+    double *P;      // p
+};
+
+// Reflector from x[0..L) (x[0] = alpha): v[0] = 1, v[i] = x[i]/(alpha - beta), tau, beta.
+// Every CTA runs it on identical data with the same reduction tree -> identical results.
+__device__ void make_reflector(const double *x, int L, double *v, double *red, double &tau, double &beta)
+{
+    double s = 0.0;
+    for (int i = 1 + threadIdx.x; i < L; i += blockDim.x) s = fma(x[i], x[i], s);
+    s = block_sum(s, red);
+    const double alpha = x[0];
+    if (s == 0.0) { tau = 0.0; beta = alpha; }
+    else {
+        beta = -copysign(sqrt(alpha * alpha + s), alpha);
+        tau = (beta - alpha) / beta;
+    }
+    const double scale = (tau == 0.0) ? 0.0 : 1.0 / (alpha - beta);
+    for (int i = threadIdx.x; i < L; i += blockDim.x) v[i] = (i == 0) ? 1.0 : x[i] * scale;
+    __syncthreads();
+}
+
+// One grid barrier per column: column g of the trailing matrix is owned by warp g mod
+// (#warps) for the whole reduction, so the owner's update of step j and its product with
+// v_{j+1} for step j+1 are fused (each column read and written once per step); only the
+// vector P = tau A2 v crosses CTAs.  Column j+1 -- the source of the next reflector -- is
+// not written in step j; every CTA applies step j's rank-2 update to it privately.
+__global__ void __launch_bounds__(256)
+tridiag_kernel(TridArgs a)
+{
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sm[];
+    const int p = a.p;
+    double *v = sm, *vn = sm + p, *w = sm + 2 * p, *c = sm + 3 * p;
+    __shared__ double red[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int gw = blockIdx.x * nwb + wid, nwg = gridDim.x * nwb;
+    double *A = a.A;
+    if (p <= 2) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.d[0] = A[0];
+            if (p == 2) { a.e[0] = A[1]; a.d[1] = A[3]; a.tau[0] = 0.0; }
+        }
+        return;
+    }
+    // prologue: reflector 0 from column 0 (rows 1..p-1), products for step 0
+    double tau, beta;
+    make_reflector(A + 1, p - 1, v, red, tau, beta);
+    for (int g = 1 + gw; g < p; g += nwg) {
+        const double *col = A + (long)g * p + 1;
+        double s = 0.0;
+        for (int i = lane; i < p - 1; i += 32) s = fma(col[i], v[i], s);
+        s = warp_sum(s);
+        if (lane == 0) a.P[g] = tau * s;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.d[0] = A[0];
+    grid.sync();
+    for (int j = 0; j + 2 < p; j++) {
+        const int L = p - j - 1;                 // rows j+1 .. p-1
+        const int r0 = j + 1;
+        // (c) w = P - (tau/2)(P.v) v     (all CTAs, identical)
+        double k = 0.0;
+        for (int i = threadIdx.x; i < L; i += blockDim.x) { double t = a.P[r0 + i]; w[i] = t; k = fma(t, v[i], k); }
+        k = 0.5 * tau * block_sum(k, red);
+        for (int i = threadIdx.x; i < L; i += blockDim.x) w[i] = fma(-k, v[i], w[i]);
+        __syncthreads();
+        // (e) updated column j+1 (private copy), next reflector from rows j+2..
+        const double *cj = A + (long)r0 * p + r0;
+        for (int i = threadIdx.x; i < L; i += blockDim.x) c[i] = cj[i] - v[i] * w[0] - w[i] * v[0];
+        __syncthreads();
+        double taun = 0.0, betan = 0.0;
+        const bool more = (j + 3 < p);
+        if (more) make_reflector(c + 1, L - 1, vn, red, taun, betan);
+        if (blockIdx.x == 0) {
+            for (int i = threadIdx.x; i < L; i += blockDim.x) a.R[(long)j * p + r0 + i] = v[i];
+            if (threadIdx.x == 0) {
+                a.e[j] = beta; a.tau[j] = tau; a.d[j + 1] = c[0];
+                if (!more) { a.e[j + 1] = c[1]; a.tau[j + 1] = 0.0; }
+            }
+        }
+        // (d) owners: update columns g >= j+2 and, fused, P_{j+1}[g] = taun * col_g' . vn
+        for (int g = r0 + 1 + gw; g < p; g += nwg) {
+            double *col = A + (long)g * p + r0;
+            const int ig = g - r0;
+            const double vg = v[ig], wg = w[ig];
+            double s = 0.0;
+            for (int i = 1 + lane; i < L; i += 32) {
+                double x = col[i] - v[i] * wg - w[i] * vg;
+                col[i] = x;
+                s = fma(x, vn[i - 1], s);
+            }
+            if (more) {
+                s = warp_sum(s);
+                if (lane == 0) a.P[g] = taun * s;
+            }
+        }
+        grid.sync();
+        for (int i = threadIdx.x; i < L - 1; i += blockDim.x) v[i] = vn[i];
+        tau = taun; beta = betan;
+        __syncthreads();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.d[p - 1] = A[(long)(p - 1) * p + p - 1];
+}
+
+// (previous two-barrier version kept for reference in the git history)
+__global__ void __launch_bounds__(256)
+tridiag_kernel_2sync(TridArgs a)
+{
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sm[];
+    double *v = sm;              // p
+    double *w = sm + a.p;        // p
+    __shared__ double red[32];
+    __shared__ double s_tau, s_beta;
+    const int p = a.p;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int gw = blockIdx.x * nwb + wid, nwg = gridDim.x * nwb;
+    double *A = a.A;
+    for (int j = 0; j + 2 < p; j++) {
+        const int L = p - j - 1;
+        const double *x = A + (long)j * p + j + 1;        // column j, rows j+1..p-1
+        double s = 0.0;
+        for (int i = 1 + threadIdx.x; i < L; i += blockDim.x) { double t = x[i]; v[i] = t; s = fma(t, t, s); }
+        s = block_sum(s, red);
+        if (threadIdx.x == 0) {
+            double alpha = x[0];
+            if (s == 0.0) { s_tau = 0.0; s_beta = alpha; }
+            else {
+                double beta = -copysign(sqrt(alpha * alpha + s), alpha);
+                s_tau = (beta - alpha) / beta;
+                s_beta = beta;
+                v[0] = alpha - beta;            // scale factor stored temporarily
+            }
+        }
+        __syncthreads();
+        const double tau = s_tau;
+        if (blockIdx.x == 0 && threadIdx.x == 0) { a.d[j] = A[(long)j * p + j]; a.e[j] = s_beta; a.tau[j] = tau; }
+        if (tau == 0.0) {
+            if (blockIdx.x == 0)        // reflector column j = 0 below the subdiagonal
+                for (int i = 1 + threadIdx.x; i < L; i += blockDim.x) A[(long)j * p + j + 1 + i] = 0.0;
+            grid.sync();
+            continue;
+        }
+        const double scale = 1.0 / v[0];
+        __syncthreads();
+        for (int i = threadIdx.x; i < L; i += blockDim.x) v[i] = (i == 0) ? 1.0 : v[i] * scale;
+        __syncthreads();
+        // p = tau * A2 v, column-distributed (A2 symmetric: row r = column r)
+        double *A2 = A + (long)(j + 1) * p + (j + 1);
+        for (int r = gw; r < L; r += nwg) {
+            const double *col = A2 + (long)r * p;
+            double dsum = 0.0;
+            for (int i = lane; i < L; i += 32) dsum = fma(col[i], v[i], dsum);
+            dsum = warp_sum(dsum);
+            if (lane == 0) a.P[r] = tau * dsum;
+        }
+        grid.sync();
+        double k = 0.0;
+        for (int i = threadIdx.x; i < L; i += blockDim.x) { double t = a.P[i]; w[i] = t; k = fma(t, v[i], k); }
+        k = 0.5 * tau * block_sum(k, red);
+        for (int i = threadIdx.x; i < L; i += blockDim.x) w[i] = fma(-k, v[i], w[i]);
+        __syncthreads();
+        for (int r = gw; r < L; r += nwg) {
+            double *col = A2 + (long)r * p;
+            const double vr = v[r], wr = w[r];
+            for (int i = lane; i < L; i += 32) col[i] = col[i] - v[i] * wr - w[i] * vr;
+        }
+        if (blockIdx.x == 0)            // store v[1..] below the subdiagonal of column j
+            for (int i = 1 + threadIdx.x; i < L; i += blockDim.x) A[(long)j * p + j + 1 + i] = v[i];
+        grid.sync();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (p >= 2) {
+            a.d[p - 2] = A[(long)(p - 2) * p + p - 2];
+            a.e[p - 2] = A[(long)(p - 2) * p + p - 1];
+            a.tau[p - 2] = 0.0;
+        }
+        a.d[p - 1] = A[(long)(p - 1) * p + p - 1];
+    }
+}
+
+// ---------------------------------------------------------------- 2. divide and conquer
+// Leaf: dense eigendecomposition of the tridiagonal block [lo, hi) (size <= 32) by
+// cyclic Jacobi in one warp; eigenvalues ascending into lam, vectors into Q block.
+__global__ void __launch_bounds__(32)
+dc_leaf_kernel(int p, const int *__restrict__ bounds, const double *__restrict__ d, const double *__restrict__ e,
+               double *__restrict__ lam, double *__restrict__ Q)
+{
+    __shared__ double M[32][33], V[32][33];
+    const int lo = bounds[blockIdx.x], hi = bounds[blockIdx.x + 1], n = hi - lo;
+    const int t = threadIdx.x;
+    for (int r = 0; r < 32; r++) {
+        double mv = 0.0;
+        if (t < n && r < n) {
+            if (r == t) mv = d[lo + r];
+            else if (r == t + 1) mv = e[lo + t];
+            else if (t == r + 1) mv = e[lo + r];
+        }
+        M[r][t] = mv;
+        V[r][t] = (r == t) ? 1.0 : 0.0;
+    }
+    __syncwarp();
+    double fro = 0.0;
+    for (int r = 0; r < n; r++) if (t < n) fro += M[r][t] * M[r][t];
+    fro = sqrt(warp_sum(fro));
+    for (int sweep = 0; sweep < 40; sweep++) {
+        double off = 0.0;
+        for (int r = 0; r < n; r++) if (t < n && r != t) off += M[r][t] * M[r][t];
+        off = sqrt(warp_sum(off));
+        if (off <= 0x1p-53 * fro || off == 0.0) break;
+        for (int pp = 0; pp < n - 1; pp++)
+            for (int q = pp + 1; q < n; q++) {
+                double apq = M[pp][q];
+                if (apq == 0.0) continue;
+                double app = M[pp][pp], aqq = M[q][q];
+                double tt = (aqq - app) / (2.0 * apq);
+                double tn = isinf(tt) ? 0.0 : ((tt >= 0.0) ? 1.0 : -1.0) / (fabs(tt) + sqrt(1.0 + tt * tt));
+                double c = 1.0 / sqrt(1.0 + tn * tn), s = tn * c;
+                __syncwarp();
+                if (t < n) {           // columns pp, q of row t
+                    double a1 = M[t][pp], a2 = M[t][q];
+                    M[t][pp] = c * a1 - s * a2; M[t][q] = s * a1 + c * a2;
+                }
+                __syncwarp();
+                if (t < n) {           // rows pp, q of column t
+                    double a1 = M[pp][t], a2 = M[q][t];
+                    M[pp][t] = c * a1 - s * a2; M[q][t] = s * a1 + c * a2;
+                    double v1 = V[t][pp], v2 = V[t][q];
+                    V[t][pp] = c * v1 - s * v2; V[t][q] = s * v1 + c * v2;
+                }
+                __syncwarp();
+                if (t == 0) { M[pp][q] = 0.0; M[q][pp] = 0.0; }
+                __syncwarp();
+            }
+    }
+    // sort ascending (rank by comparison)
+    if (t < n) {
+        double dt = M[t][t];
+        int rank = 0;
+        for (int r = 0; r < n; r++) { double dr = M[r][r]; if (dr < dt || (dr == dt && r < t)) rank++; }
+        lam[lo + rank] = dt;
+        for (int r = 0; r < n; r++) Q[(long)(lo + rank) * p + lo + r] = V[r][t];
+    }
+}
+
+struct MergeInfo { int lo, mid, hi; };
+
+// M1: z, sort, deflation scan.  One CTA per merge.
+//   out (per merge, indexed from lo): perm (sorted position -> local column),
+//   Ds (sorted, deflation-modified), zK/DK (non-deflated compressed), K (positions),
+//   defl positions; rot list; counts[2*m] = kk, counts[2*m+1] = nrot.
+__global__ void __launch_bounds__(1024)
+dc_merge_prep_kernel(int p, const MergeInfo *__restrict__ mi, const double *__restrict__ e,
+                     const double *__restrict__ lam, const double *__restrict__ Q,
+                     int *__restrict__ perm, double *__restrict__ Ds, double *__restrict__ zs,
+                     double *__restrict__ DK, double *__restrict__ zK, int *__restrict__ Kpos,
+                     int *__restrict__ Dpos, double *__restrict__ rot, int *__restrict__ counts,
+                     double *__restrict__ rho_out)
+{
+    __shared__ double red[32];
+    const MergeInfo m = mi[blockIdx.x];
+    const int lo = m.lo, mid = m.mid, hi = m.hi, n = hi - lo, n1 = mid - lo;
+    const double rho_raw = e[mid - 1];
+    const double sgn = (rho_raw < 0.0) ? -1.0 : 1.0;
+    const double rho = 2.0 * fabs(rho_raw);
+    const double isq2 = 0.70710678118654752440;
+    // merge-sort positions: element i of child 1 (lam[lo+i]) and child 2 (lam[mid+i])
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double val = lam[lo + i];
+        int pos;
+        if (i < n1) {           // count elements of child 2 strictly smaller
+            int a = 0, b = n - n1;
+            while (a < b) { int c = (a + b) >> 1; if (lam[mid + c] < val) a = c + 1; else b = c; }
+            pos = i + a;
+        } else {                // count elements of child 1 <= val
+            int a = 0, b = n1;
+            while (a < b) { int c = (a + b) >> 1; if (lam[lo + c] <= val) a = c + 1; else b = c; }
+            pos = (i - n1) + a;
+        }
+        perm[lo + pos] = i;
+        Ds[lo + pos] = val;
+        double z = (i < n1) ? Q[(long)(lo + i) * p + (mid - 1)] : sgn * Q[(long)(lo + i) * p + mid];
+        zs[lo + pos] = z * isq2;
+    }
+    __syncthreads();
+    double mx = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) mx = fmax(mx, fmax(fabs(Ds[lo + i]), fabs(zs[lo + i])));
+    mx = block_max(mx, red);
+    if (threadIdx.x == 0) {
+        const double tol = 8.0 * 0x1p-52 * mx;
+        int kk = 0, nd = 0, nr = 0, prev = -1;
+        for (int k = 0; k < n; k++) {
+            if (rho * fabs(zs[lo + k]) <= tol) { Dpos[lo + nd++] = k; continue; }
+            if (prev < 0) { prev = k; continue; }
+            double s = zs[lo + prev], c = zs[lo + k];
+            double tau = hypot(c, s);
+            double t = Ds[lo + k] - Ds[lo + prev];
+            c /= tau; s = -s / tau;
+            if (fabs(t * c * s) <= tol) {
+                zs[lo + k] = tau; zs[lo + prev] = 0.0;
+                rot[4 * (lo + nr) + 0] = prev; rot[4 * (lo + nr) + 1] = k;
+                rot[4 * (lo + nr) + 2] = c; rot[4 * (lo + nr) + 3] = s;
+                nr++;
+                double tp = Ds[lo + prev] * c * c + Ds[lo + k] * s * s;
+                Ds[lo + k] = Ds[lo + prev] * s * s + Ds[lo + k] * c * c;
+                Ds[lo + prev] = tp;
+                Dpos[lo + nd++] = prev;
+                prev = k;
+            } else {
+                Kpos[lo + kk++] = prev;
+                prev = k;
+            }
+        }
+        if (prev >= 0) Kpos[lo + kk++] = prev;
+        counts[2 * blockIdx.x] = kk;
+        counts[2 * blockIdx.x + 1] = nr;
+        rho_out[blockIdx.x] = rho;
+    }
+    __syncthreads();
+    const int kk = counts[2 * blockIdx.x];
+    for (int i = threadIdx.x; i < kk; i += blockDim.x) {
+        DK[lo + i] = Ds[lo + Kpos[lo + i]];
+        zK[lo + i] = zs[lo + Kpos[lo + i]];
+    }
+}
+
+// M2: gather Q block columns into sorted order (Qg[:, lo+k] = Q[:, lo+perm[k]], rows lo..hi),
+// apply the deflation rotations in order (each thread one row), and compact the
+// non-deflated columns into Qk[:, lo+k] = Qg[:, lo+Kpos[k]].
+__global__ void dc_gather_rotate_kernel(int p, const MergeInfo *__restrict__ mi, const double *__restrict__ Q,
+                                        const int *__restrict__ perm, const double *__restrict__ rot,
+                                        const int *__restrict__ counts, const int *__restrict__ Kpos,
+                                        double *__restrict__ Qg, double *__restrict__ Qk)
+{
+    const MergeInfo m = mi[blockIdx.y];
+    const int lo = m.lo, n = m.hi - m.lo;
+    const int kk = counts[2 * blockIdx.y], nr = counts[2 * blockIdx.y + 1];
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        for (int k = 0; k < n; k++) Qg[(long)(lo + k) * p + lo + r] = Q[(long)(lo + perm[lo + k]) * p + lo + r];
+        for (int t = 0; t < nr; t++) {
+            const double *R = rot + 4 * (lo + t);
+            int a = (int)R[0], b = (int)R[1];
+            double c = R[2], s = R[3];
+            double *xa = Qg + (long)(lo + a) * p + lo + r, *xb = Qg + (long)(lo + b) * p + lo + r;
+            double x = *xa, y = *xb;
+            *xa = c * x + s * y;
+            *xb = c * y - s * x;
+        }
+        for (int k = 0; k < kk; k++) Qk[(long)(lo + k) * p + lo + r] = Qg[(long)(lo + Kpos[lo + k]) * p + lo + r];
+    }
+}
+
+// M3: secular roots by bisection around the nearer pole.  Thread per root.
+__global__ void dc_secular_kernel(const MergeInfo *__restrict__ mi, const double *__restrict__ DK,
+                                  const double *__restrict__ zK, const int *__restrict__ counts,
+                                  const double *__restrict__ rho_in, double *__restrict__ taus,
+                                  int *__restrict__ orig)
+{
+    const MergeInfo m = mi[blockIdx.y];
+    const int lo = m.lo;
+    const int kk = counts[2 * blockIdx.y];
+    const double rho = rho_in[blockIdx.y];
+    // one warp per root: the secular sum is split across the lanes
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const double *D = DK + lo, *z = zK + lo;
+    double zz = 0.0;
+    for (int i = lane; i < kk; i += 32) zz = fma(z[i], z[i], zz);
+    zz = warp_sum(zz);
+    for (int j = gw; j < kk; j += nw) {
+        const double dl = D[j];
+        const double du = (j + 1 < kk) ? D[j + 1] : D[j] + rho * zz;
+        // choose the origin by the sign of f at the midpoint
+        int o = j;
+        if (j + 1 < kk) {
+            const double mid = 0.5 * (du - dl);
+            double f = 0.0;
+            for (int i = lane; i < kk; i += 32) f += z[i] * z[i] / ((D[i] - dl) - mid);
+            f = 1.0 + rho * warp_sum(f);
+            if (f < 0.0) o = j + 1;          // root in (mid, du): measure from the upper pole
+        }
+        const double Do = D[o];
+        double a, b;                          // tau interval
+        if (o == j) { a = 0.0; b = (j + 1 < kk) ? 0.5 * (du - dl) : du - dl; }
+        else { a = -(0.5 * (du - dl)); b = 0.0; }
+        for (int it = 0; it < 400; it++) {
+            double c = 0.5 * (a + b);
+            if (c == a || c == b) break;
+            double f = 0.0;
+            for (int i = lane; i < kk; i += 32) f += z[i] * z[i] / ((D[i] - Do) - c);
+            f = 1.0 + rho * warp_sum(f);
+            if (f > 0.0) b = c; else a = c;
+        }
+        if (lane == 0) { taus[lo + j] = 0.5 * (a + b); orig[lo + j] = o; }
+    }
+}
+
+// M4: Loewner z-hat and the unnormalised eigenvector matrix U (kk x kk, at [lo,lo]).
+__global__ void dc_vectors_kernel(int p, const MergeInfo *__restrict__ mi, const double *__restrict__ DK,
+                                  const double *__restrict__ zK, const int *__restrict__ counts,
+                                  const double *__restrict__ rho_in, const double *__restrict__ taus,
+                                  const int *__restrict__ orig, double *__restrict__ zhat, double *__restrict__ U)
+{
+    const MergeInfo m = mi[blockIdx.y];
+    const int lo = m.lo;
+    const int kk = counts[2 * blockIdx.y];
+    const double rho = rho_in[blockIdx.y];
+    const double *D = DK + lo;
+    // phase A: zhat (thread per i); phase B needs all zhat -> done in a second launch
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kk; i += gridDim.x * blockDim.x) {
+        // zhat_i^2 = (lambda_{kk-1} - d_i)/rho * prod_{j<i} (lambda_j - d_i)/(d_j - d_i)
+        //            * prod_{i<=j<kk-1} (lambda_j - d_i)/(d_{j+1} - d_i)
+        const double di = D[i];
+        auto lmd = [&](int j) { return (D[orig[lo + j]] - di) + taus[lo + j]; };
+        double prod = lmd(kk - 1) / rho;
+        for (int j = 0; j < i; j++) prod *= lmd(j) / (D[j] - di);
+        for (int j = i; j < kk - 1; j++) prod *= lmd(j) / (D[j + 1] - di);
+        double zh = sqrt(fabs(prod));
+        zhat[lo + i] = copysign(zh, zK[lo + i]);
+    }
+}
+
+__global__ void dc_umatrix_kernel(int p, const MergeInfo *__restrict__ mi, const double *__restrict__ DK,
+                                  const int *__restrict__ counts, const double *__restrict__ taus,
+                                  const int *__restrict__ orig, const double *__restrict__ zhat,
+                                  double *__restrict__ U)
+{
+    const MergeInfo m = mi[blockIdx.y];
+    const int lo = m.lo;
+    const int kk = counts[2 * blockIdx.y];
+    const double *D = DK + lo;
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int j = gw; j < kk; j += nw) {          // warp per eigenvector j
+        const double Dj = D[orig[lo + j]], tj = taus[lo + j];
+        double ss = 0.0;
+        for (int i = lane; i < kk; i += 32) {
+            double u = zhat[lo + i] / ((D[i] - Dj) - tj);
+            U[(long)(lo + j) * p + lo + i] = u;
+            ss = fma(u, u, ss);
+        }
+        ss = warp_sum(ss);
+        const double inv = 1.0 / sqrt(ss);
+        for (int i = lane; i < kk; i += 32) U[(long)(lo + j) * p + lo + i] *= inv;
+    }
+}
+
+// M6: eigenvalues of the merged block and assembly of the (unsorted) columns:
+// columns 0..kk-1: computed by GEMM into Qn; deflated columns copied; then sort.
+__global__ void dc_finish_kernel(int p, const MergeInfo *__restrict__ mi, const double *__restrict__ Ds,
+                                 const double *__restrict__ DK, const int *__restrict__ counts,
+                                 const double *__restrict__ taus, const int *__restrict__ orig,
+                                 const int *__restrict__ Dpos, const double *__restrict__ Qg,
+                                 double *__restrict__ Qn, double *__restrict__ lamtmp)
+{
+    const MergeInfo m = mi[blockIdx.y];
+    const int lo = m.lo, n = m.hi - m.lo;
+    const int kk = counts[2 * blockIdx.y];
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        if (t < kk) {
+            lamtmp[lo + t] = DK[lo + orig[lo + t]] + taus[lo + t];
+        } else {
+            int k = Dpos[lo + (t - kk)];
+            lamtmp[lo + t] = Ds[lo + k];
+            for (int r = 0; r < n; r++) Qn[(long)(lo + t) * p + lo + r] = Qg[(long)(lo + k) * p + lo + r];
+        }
+    }
+}
+
+// sort the n eigenvalues ascending (rank by comparison) and permute columns into Q
+__global__ void dc_sort_kernel(int p, const MergeInfo *__restrict__ mi, const double *__restrict__ lamtmp,
+                               const double *__restrict__ Qn, double *__restrict__ lam, double *__restrict__ Q)
+{
+    const MergeInfo m = mi[blockIdx.y];
+    const int lo = m.lo, n = m.hi - m.lo;
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int t = gw; t < n; t += nw) {
+        double v = lamtmp[lo + t];
+        int rank = 0;
+        for (int s = lane; s < n; s += 32) { double u = lamtmp[lo + s]; if (u < v || (u == v && s < t)) rank++; }
+        rank = warp_sum(rank);
+        if (lane == 0) lam[lo + rank] = v;
+        for (int r = lane; r < n; r += 32) Q[(long)(lo + rank) * p + lo + r] = Qn[(long)(lo + t) * p + lo + r];
+    }
+}
+
+// ---------------------------------------------------------------- 3. back-transformation
+// V panel (p x jb) of reflectors j0..j0+jb-1: V[:, jj] = [0..0, 1 (row j+1), A[j+2:, j]]
+__global__ void bt_panel_kernel(int p, int j0, int jb, const double *__restrict__ A, const double *__restrict__ tau,
+                                double *__restrict__ V, double *__restrict__ Tp)
+{
+    __shared__ double G[32][33];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (long idx = tid; idx < (long)p * jb; idx += nt) {
+        int i = (int)(idx % p), jj = (int)(idx / p), j = j0 + jj;
+        double v = 0.0;
+        if (i == j + 1) v = 1.0;
+        else if (i > j + 1) v = A[(long)j * p + i];
+        if (tau[j] == 0.0) v = 0.0;
+        V[idx] = v;
+    }
+    __syncthreads();
+    const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+    for (int q = w; q < jb * jb; q += nw) {
+        int a = q / jb, c = q % jb;
+        double s = 0.0;
+        if (a <= c) {
+            for (int i = lane; i < p; i += 32) s = fma(V[(long)a * p + i], V[(long)c * p + i], s);
+            s = warp_sum(s);
+        }
+        if (lane == 0) G[a][c] = s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double T[32][32];
+        for (int a = 0; a < 32; a++) for (int c = 0; c < 32; c++) T[a][c] = 0.0;
+        for (int c = 0; c < jb; c++) {
+            double tc = tau[j0 + c];
+            T[c][c] = tc;
+            for (int a = 0; a < c; a++) {
+                double sacc = 0.0;
+                for (int l = a; l < c; l++) sacc += T[a][l] * G[l][c];
+                T[a][c] = -tc * sacc;
+            }
+        }
+        for (int a = 0; a < 32; a++) for (int c = 0; c < 32; c++) Tp[a + c * 32] = T[a][c];
+    }
+}
+
+// eigenvalues descending + sign normalisation (largest |component| positive, lowest index)
+__global__ void eigfinal_kernel(int p, const double *__restrict__ lam, const double *__restrict__ X,
+                                double *__restrict__ w, double *__restrict__ V)
+{
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int j = gw; j < p; j += nw) {
+        const int src = p - 1 - j;
+        double bv = -1.0; int bi = p;
+        for (int k = lane; k < p; k += 32) {
+            double v = fabs(X[(long)src * p + k]);
+            if (v > bv || (v == bv && k < bi)) { bv = v; bi = k; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+            int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; }
+        }
+        const double sg = (X[(long)src * p + bi] < 0.0) ? -1.0 : 1.0;
+        if (lane == 0) w[j] = lam[src];
+        for (int k = lane; k < p; k += 32) V[(long)j * p + k] = sg * X[(long)src * p + k];
+    }
+}
+
+__global__ void symmetrize_copy_kernel(int p, const double *__restrict__ Ain, double *__restrict__ A)
+{
+    long tot = (long)p * p;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < tot; idx += (long)gridDim.x * blockDim.x) {
+        int i = (int)(idx % p), j = (int)(idx / p);
+        A[idx] = 0.5 * (Ain[idx] + Ain[(long)i * p + j]);
+    }
+}
+
+__global__ void zero_d_kernel(long len, double *x)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < len; i += (long)gridDim.x * blockDim.x) x[i] = 0.0;
+}
+
+// ---------------------------------------------------------------- driver
+int SyevdWork::alloc(int pmax_) {
+    pmax = pmax_;
+    size_t pp = (size_t)pmax * pmax;
+    for (double **b : {&A, &Q, &Qg, &Qk, &U, &Qn, &R}) LYAP_CUDA_TRY(cudaMalloc(b, sizeof(double) * pp));
+    LYAP_CUDA_TRY(cudaMalloc(&vec, sizeof(double) * (size_t)pmax * 16 + 32 * 33 * 64 * 8));
+    LYAP_CUDA_TRY(cudaMalloc(&ivec, sizeof(int) * (size_t)pmax * 8 + 4096));
+    LYAP_CUDA_TRY(cudaMalloc(&rot, sizeof(double) * (size_t)pmax * 4));
+    return LYAP_OK;
+}
+void SyevdWork::release() {
+    for (double *b : {A, Q, Qg, Qk, U, Qn, R, vec, rot}) cudaFree(b);
+    cudaFree(ivec);
+    A = Q = Qg = Qk = U = Qn = R = vec = rot = nullptr;
+    ivec = nullptr;
+}
+
+int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V_out, SyevdWork &W)
+{
+    if (p > W.pmax) return LYAP_ERR_CAPACITY;
+    const size_t pp = (size_t)p * p;
+    double *d = W.vec, *e = d + p, *tau = e + p, *P = tau + p, *lam = P + p, *Ds = lam + p, *zs = Ds + p,
+           *DK = zs + p, *zK = DK + p, *taus = zK + p, *zhat = taus + p, *lamtmp = zhat + p, *rho = lamtmp + p,
+           *Tp = rho + p;
+    int *perm = W.ivec, *Kpos = perm + p, *Dpos = Kpos + p, *orig = Dpos + p, *counts = orig + p,
+        *bounds = counts + 2 * p;
+    MergeInfo *mi = reinterpret_cast<MergeInfo *>(bounds + p + 2);
+    const int gsz = std::min(ceil_div((long)pp, 256), 2048);
+    static int prof = -1;
+    static cudaEvent_t pev[4];
+    if (prof < 0) {
+        const char *ev = getenv("LYAP_PROFILE_EIG");
+        prof = (ev && ev[0] == '1') ? 1 : 0;
+        if (prof) for (auto &x : pev) cudaEventCreate(&x);
+    }
+    if (prof) cudaEventRecord(pev[0], s);
+    // 1. tridiagonalisation (reflectors stay in W.A until the back-transformation)
+    symmetrize_copy_kernel<<<gsz, 256, 0, s>>>(p, Ain, W.A);
+    LYAP_TRY(launched());
+    {
+        static int max_blocks = 0;
+        const size_t smem = sizeof(double) * 4 * (size_t)W.pmax;
+        if (smem > 200 * 1024) return LYAP_ERR_CAPACITY;
+        if (max_blocks == 0) {
+            int dev, nsm, per = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tridiag_kernel, 256, smem);
+            max_blocks = nsm * std::max(1, std::min(per, 1));
+        }
+        int grid = std::min(max_blocks, std::max(1, p / 4));
+        TridArgs ta{p, W.A, W.R, d, e, tau, P};
+        void *args[] = {&ta};
+        LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)tridiag_kernel, dim3(grid), dim3(256), args, smem, s));
+        LYAP_TRY(launched());
+    }
+    if (prof) cudaEventRecord(pev[1], s);
+    // 2. divide and conquer on (d, e): leaves of size <= 32, power-of-two tree
+    int nl = 1;
+    while ((p + nl - 1) / nl > 32) nl *= 2;
+    std::vector<int> hb(nl + 1);
+    for (int i = 0; i <= nl; i++) hb[i] = (int)((long)i * p / nl);
+    std::vector<double> hd(p), he(std::max(p - 1, 1));
+    LYAP_CUDA_TRY(cudaMemcpyAsync(hd.data(), d, sizeof(double) * p, cudaMemcpyDeviceToHost, s));
+    if (p > 1) LYAP_CUDA_TRY(cudaMemcpyAsync(he.data(), e, sizeof(double) * (p - 1), cudaMemcpyDeviceToHost, s));
+    LYAP_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int i = 1; i < nl; i++) {          // Cuppen tears: T = diag(T1', T2') + |e| v v^T
+        int m = hb[i];
+        double r = fabs(he[m - 1]);
+        hd[m - 1] -= r;
+        hd[m] -= r;
+    }
+    LYAP_CUDA_TRY(cudaMemcpyAsync(d, hd.data(), sizeof(double) * p, cudaMemcpyHostToDevice, s));
+    LYAP_CUDA_TRY(cudaMemcpyAsync(bounds, hb.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice, s));
+    zero_d_kernel<<<gsz, 256, 0, s>>>((long)pp, W.Q);
+    LYAP_TRY(launched());
+    dc_leaf_kernel<<<nl, 32, 0, s>>>(p, bounds, d, e, lam, W.Q);
+    LYAP_TRY(launched());
+    for (int width = 1; width < nl; width *= 2) {
+        std::vector<MergeInfo> hm;
+        for (int i = 0; i + width < nl; i += 2 * width)
+            hm.push_back({hb[i], hb[i + width], hb[std::min(i + 2 * width, nl)]});
+        const int nm = (int)hm.size();
+        LYAP_CUDA_TRY(cudaMemcpyAsync(mi, hm.data(), sizeof(MergeInfo) * nm, cudaMemcpyHostToDevice, s));
+        dc_merge_prep_kernel<<<nm, 1024, 0, s>>>(p, mi, e, lam, W.Q, perm, Ds, zs, DK, zK, Kpos, Dpos, W.rot,
+                                                 counts, rho);
+        LYAP_TRY(launched());
+        int maxn = 0;
+        for (auto &x : hm) maxn = std::max(maxn, x.hi - x.lo);
+        dim3 g1(ceil_div(maxn, 128), nm);
+        dc_gather_rotate_kernel<<<g1, 128, 0, s>>>(p, mi, W.Q, perm, W.rot, counts, Kpos, W.Qg, W.Qk);
+        LYAP_TRY(launched());
+        dc_secular_kernel<<<dim3(ceil_div((long)maxn * 32, 256), nm), 256, 0, s>>>(mi, DK, zK, counts, rho, taus, orig);
+        LYAP_TRY(launched());
+        dc_vectors_kernel<<<g1, 128, 0, s>>>(p, mi, DK, zK, counts, rho, taus, orig, zhat, W.U);
+        LYAP_TRY(launched());
+        dim3 g2(ceil_div((long)maxn * 32, 256), nm);
+        dc_umatrix_kernel<<<g2, 256, 0, s>>>(p, mi, DK, counts, taus, orig, zhat, W.U);
+        LYAP_TRY(launched());
+        std::vector<int> hc(2 * nm);
+        LYAP_CUDA_TRY(cudaMemcpyAsync(hc.data(), counts, sizeof(int) * 2 * nm, cudaMemcpyDeviceToHost, s));
+        LYAP_CUDA_TRY(cudaStreamSynchronize(s));
+        for (int q = 0; q < nm; q++) {
+            const int lo = hm[q].lo, n = hm[q].hi - hm[q].lo, kk = hc[2 * q];
+            if (kk > 0) {
+                const size_t off = (size_t)lo * p + lo;
+                LYAP_TRY(dgemm_cm(s, false, false, n, kk, kk, 1.0, W.Qk + off, p, W.U + off, p, 0.0, W.Qn + off, p));
+            }
+        }
+        dc_finish_kernel<<<g1, 128, 0, s>>>(p, mi, Ds, DK, counts, taus, orig, Dpos, W.Qg, W.Qn, lamtmp);
+        LYAP_TRY(launched());
+        dc_sort_kernel<<<g2, 256, 0, s>>>(p, mi, lamtmp, W.Qn, lam, W.Q);
+        LYAP_TRY(launched());
+    }
+    if (prof) cudaEventRecord(pev[2], s);
+    // 3. back-transformation X = Q_H Q_T: panels of 32 reflectors, last panel first
+    const int nref = std::max(p - 2, 0);
+    for (int j0 = ((nref - 1) / 32) * 32; nref > 0 && j0 >= 0; j0 -= 32) {
+        const int jb = std::min(32, nref - j0);
+        bt_panel_kernel<<<1, 512, 0, s>>>(p, j0, jb, W.R, tau, W.Qg, Tp);
+        LYAP_TRY(launched());
+        // Wt = V^T X (jb x p) ; Wt2 = T Wt ; X -= V Wt2    (V = W.Qg, p x jb)
+        LYAP_TRY(dgemm_cm(s, true, false, jb, p, p, 1.0, W.Qg, p, W.Q, p, 0.0, W.Qk, 32));
+        LYAP_TRY(gemm_strided<double, double, double, double>(s, jb, p, jb, 1.0, Tp, 1, 32, W.Qk, 1, 32, 0.0,
+                                                              W.U, 1, 32));
+        LYAP_TRY(dgemm_cm(s, false, false, p, p, jb, -1.0, W.Qg, p, W.U, 32, 1.0, W.Q, p));
+    }
+    eigfinal_kernel<<<std::min(ceil_div((long)p * 32, 256), 1024), 256, 0, s>>>(p, lam, W.Q, w_out, V_out);
+    LYAP_TRY(launched());
+    if (prof) {
+        cudaEventRecord(pev[3], s);
+        cudaEventSynchronize(pev[3]);
+        float a = 0, b = 0, c = 0;
+        cudaEventElapsedTime(&a, pev[0], pev[1]);
+        cudaEventElapsedTime(&b, pev[1], pev[2]);
+        cudaEventElapsedTime(&c, pev[2], pev[3]);
+        fprintf(stderr, "lyap: syevd p=%d tridiag %.3f ms  d&c %.3f ms  backtransform %.3f ms\n", p, a, b, c);
+    }
+    return LYAP_OK;
+}
+
+}  // namespace lyap

@@ -97,6 +97,48 @@ def test_syev_parity(gpu, orc, n):
     assert np.allclose(V.cpu().numpy(), Vo, atol=1e-9)
 
 
+def _eig_checks(A, w, V, tol=1e-12):
+    n = A.shape[0]
+    scale = max(np.abs(np.linalg.eigvalsh(A)).max(), 1e-300)
+    wr = np.linalg.eigvalsh(A)[::-1]
+    assert np.allclose(w, wr, atol=tol * scale * max(1, n / 100))
+    assert np.linalg.norm(V.T @ V - np.eye(n)) <= tol * n
+    assert np.linalg.norm(A @ V - V * w[None, :]) <= tol * scale * n
+
+
+@pytest.mark.parametrize("n", [33, 64, 131, 300, 700])
+def test_syevd_random(gpu, n):
+    """Tridiagonalisation + divide-and-conquer path (n > 32) against numpy eigh and
+    the defining identities A V = V diag(w), V^T V = I."""
+    B = np.random.default_rng(n + 5).standard_normal((n, n))
+    A = B + B.T
+    w, V = gpu.syev(cuda(A))
+    _eig_checks(A, w.cpu().numpy(), V.cpu().numpy())
+
+
+@pytest.mark.parametrize("kind", ["graded", "clustered", "lowrank", "indefinite_pm"])
+def test_syevd_hard_spectra(gpu, kind):
+    """Spectra like the IR's kernel matrices: eigenvalues spanning 15 decades, clusters,
+    exact zero blocks (heavy deflation), and +/- pairs."""
+    n = 257
+    rng = np.random.default_rng(9)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    if kind == "graded":
+        lam = np.sign(rng.standard_normal(n)) * 10.0 ** (-15 * rng.uniform(0, 1, n))
+    elif kind == "clustered":
+        lam = np.repeat([1.0, 1e-3, -2.0, 5e-9], [60, 70, 60, 67]) * (1 + 1e-14 * rng.standard_normal(n))
+    elif kind == "lowrank":
+        lam = np.zeros(n)
+        lam[:10] = rng.uniform(1, 2, 10)
+    else:
+        x = rng.uniform(0.1, 1, n // 2)
+        lam = np.concatenate([x, -x, [0.5]])
+    A = (Q * lam[None, :]) @ Q.T
+    A = (A + A.T) / 2
+    w, V = gpu.syev(cuda(A))
+    _eig_checks(A, w.cpu().numpy(), V.cpu().numpy(), tol=1e-12)
+
+
 def test_rank_trunc_chol_parity(gpu, orc):
     rng = np.random.default_rng(3)
     n, c = 200, 40
