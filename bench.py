@@ -38,7 +38,7 @@ UNIT = "solves/s"
 WORKLOADS = {
     "cfg0": dict(gen="cfg0", us="fp16", tol=1e-14, maxit=10, max_cols=128,
                  desc="configs[0]: n=64 m=2 Cholesky W=LL^T, A=Q diag(-lambda) Q^T, fp16 solver, tol 1e-14"),
-    "cfg1": dict(gen="cfg1", us="bf16", tol=1e-14, maxit=50, max_cols=256,
+    "cfg1": dict(gen="cfg1", us="bf16", tol=1e-14, maxit=50, max_cols=640,
                  desc="configs[1]: n=1024 m=4 LDL^T W=LSL^T, A=-(Q diag(lambda) Q^T)+K, bf16 solver, "
                       "fp64 refinement, tol 1e-14"),
     "cfg2": dict(gen="cfg2", us="fp16", tol=1e-14, maxit=50, max_cols=512,

@@ -8,6 +8,7 @@
 // Skinny products (few output tiles, long K) are split along K into a
 // workspace and reduced in a fixed order (deterministic).
 #pragma once
+#include <type_traits>
 #include "common.cuh"
 
 namespace lyap {
@@ -111,12 +112,112 @@ inline void *splitk_workspace(size_t bytes) {
     return ptr;
 }
 
+// ---------------------------------------------------------------- fp64 on the DMMA pipe
+// C tile 64 x 64 per CTA, 4 warps (2 x 2) of 32 x 32, k-tiles of 16 staged in shared
+// memory (double-buffered through registers); mma.sync.m8n8k4.f64 (the fp64 tensor
+// path of sm_100a -- tcgen05 has no f64 kind).  Fragment layouts (PTX ISA m8n8k4 .f64):
+// A: row = lane/4, k = lane%4; B: k = lane%4, col = lane/4; C: row = lane/4,
+// cols 2*(lane%4) + {0,1}.
+__device__ __forceinline__ void dmma8x8x4(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+static __global__ void __launch_bounds__(128)
+dgemm_dmma_kernel(int M, int N, int K, int kchunk, double alpha,
+                  const double *__restrict__ A, long sam, long sak,
+                  const double *__restrict__ B, long sbk, long sbn,
+                  double beta, double *__restrict__ C, long scm, long scn, double *__restrict__ work)
+{
+    constexpr int BM = 64, BN = 64, BK = 16, PAD = 4;
+    __shared__ double As[2][BK][BM + PAD];
+    __shared__ double Bs[2][BK][BN + PAD];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const long m0 = (long)blockIdx.y * BM, n0 = (long)blockIdx.x * BN;
+    const int kb = blockIdx.z * kchunk, ke = min(K, kb + kchunk);
+    const bool a_kfast = (sak == 1), b_kfast = (sbk == 1);
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+    double ra[8], rb[8];
+    auto gload = [&](int k0) {
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            int idx = tid + e * 128, mm, kk;
+            if (a_kfast) { kk = idx % BK; mm = idx / BK; } else { mm = idx % BM; kk = idx / BM; }
+            long gm = m0 + mm, gk = k0 + kk;
+            ra[e] = (gm < M && gk < ke) ? A[gm * sam + gk * sak] : 0.0;
+            int nn;
+            if (b_kfast) { kk = idx % BK; nn = idx / BK; } else { nn = idx % BN; kk = idx / BN; }
+            long gn = n0 + nn;
+            gk = k0 + kk;
+            rb[e] = (gn < N && gk < ke) ? B[gk * sbk + gn * sbn] : 0.0;
+        }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            int idx = tid + e * 128, mm, kk;
+            if (a_kfast) { kk = idx % BK; mm = idx / BK; } else { mm = idx % BM; kk = idx / BM; }
+            As[buf][kk][mm] = ra[e];
+            int nn;
+            if (b_kfast) { kk = idx % BK; nn = idx / BK; } else { nn = idx % BN; kk = idx / BN; }
+            Bs[buf][kk][nn] = rb[e];
+        }
+    };
+    const int ntiles = (ke > kb) ? (ke - kb + BK - 1) / BK : 0;
+    if (ntiles > 0) { gload(kb); sstore(0); }
+    __syncthreads();
+    const int lr = lane >> 2, lk = lane & 3;
+    for (int t = 0; t < ntiles; t++) {
+        const int buf = t & 1;
+        if (t + 1 < ntiles) gload(kb + (t + 1) * BK);
+#pragma unroll
+        for (int k4 = 0; k4 < BK; k4 += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) a[i] = As[buf][k4 + lk][wm + i * 8 + lr];
+#pragma unroll
+            for (int j = 0; j < 4; j++) b[j] = Bs[buf][k4 + lk][wn + j * 8 + lr];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) dmma8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+        if (t + 1 < ntiles) sstore(buf ^ 1);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const long gm = m0 + wm + i * 8 + lr;
+        if (gm >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+#pragma unroll
+            for (int v = 0; v < 2; v++) {
+                const long gn = n0 + wn + j * 8 + 2 * lk + v;
+                if (gn >= N) continue;
+                const double r = alpha * acc[i][j][v];
+                if (work) work[(long)blockIdx.z * M * N + gm + gn * (long)M] = r;
+                else {
+                    double *cp = C + gm * scm + gn * scn;
+                    *cp = (beta != 0.0) ? fma(beta, *cp, r) : r;
+                }
+            }
+    }
+}
+
 template <typename TA, typename TB, typename TC, typename Acc>
 int gemm_strided(cudaStream_t s, int M, int N, int K, Acc alpha,
                  const TA *A, long sam, long sak, const TB *B, long sbk, long sbn,
                  Acc beta, TC *C, long scm, long scn)
 {
     if (M <= 0 || N <= 0) return LYAP_OK;
+    constexpr bool all_f64 = std::is_same<TA, double>::value && std::is_same<TB, double>::value &&
+                             std::is_same<TC, double>::value && std::is_same<Acc, double>::value;
     constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
     const int tiles = ceil_div(N, BN) * ceil_div(M, BM);
     int splits = 1;
@@ -133,8 +234,13 @@ int gemm_strided(cudaStream_t s, int M, int N, int K, Acc alpha,
     const int kchunk = (splits > 1) ? ceil_div(ceil_div(K, splits), BK) * BK : std::max(K, 1);
     if (splits > 1) splits = ceil_div(K, kchunk);
     dim3 grid(ceil_div(N, BN), ceil_div(M, BM), splits);
-    gemm_strided_kernel<TA, TB, TC, Acc, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, s>>>(
-        M, N, K, kchunk, alpha, A, sam, sak, B, sbk, sbn, beta, C, scm, scn, splits > 1 ? work : nullptr);
+    if constexpr (all_f64) {
+        dgemm_dmma_kernel<<<grid, 128, 0, s>>>(M, N, K, kchunk, alpha, A, sam, sak, B, sbk, sbn, beta, C, scm,
+                                               scn, splits > 1 ? work : nullptr);
+    } else {
+        gemm_strided_kernel<TA, TB, TC, Acc, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, s>>>(
+            M, N, K, kchunk, alpha, A, sam, sak, B, sbk, sbn, beta, C, scm, scn, splits > 1 ? work : nullptr);
+    }
     LYAP_TRY(launched());
     if (splits > 1) {
         int g = std::min(ceil_div((long)M * N, 256), 2048);

@@ -2,10 +2,12 @@
 // "Compute a thin QR decomposition F_i = U_i T_i", PAPER.md l.164, l.239,
 // l.789, l.823; the error analysis l.357 assumes Householder QR).
 //
-// Blocked right-looking Householder with compact-WY panels of width 16:
-//   panel kernel (one CTA): reflectors H_j = I - tau_j v_j v_j^T,
-//     v_j = x - alpha e_1, alpha = -sign(x_1)||x||, tau_j = 2 / v_j^T v_j,
-//     plus the panel's triangular factor T (H_0..H_{b-1} = I - V T V^T);
+// Blocked right-looking Householder with compact-WY panels of width 32:
+//   panel kernel (one CTA, panel staged in shared memory when it fits):
+//     reflectors H_j = I - tau_j v_j v_j^T, v_j = x - alpha e_1,
+//     alpha = -sign(x_1)||x||, tau_j = 2 / v_j^T v_j; the reflector is applied
+//     to the remaining panel columns one warp per column; then the panel's
+//     triangular factor T (H_0..H_{b-1} = I - V T V^T);
 //   trailing update W <- W - V (T^T (V^T W)) with the strided GEMM;
 //   Q = H_0 ... H_{k-1} [I_k; 0] accumulated backwards the same way.
 // The sign convention diag(R) >= 0 makes the factorization unique for full
@@ -13,95 +15,128 @@
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "lyap_internal.h"
+#include "ktimer.h"
 
 namespace lyap {
 
-static constexpr int QB = 16;
+static constexpr int QB = 32;
 
 // Factor panel columns [j0, j0+jb) of W (m x n, ld m), rows j0..m-1.
 // Writes V (m x k, ld m; zero above the diagonal), tau, and T_panel (QB x QB).
 __global__ void __launch_bounds__(512)
 qr_panel_kernel(int m, int j0, int jb, double *__restrict__ W, double *__restrict__ V,
-                double *__restrict__ tau, double *__restrict__ Tp)
+                double *__restrict__ tau, double *__restrict__ Tp, int use_smem)
 {
+    extern __shared__ double smp[];
     __shared__ double red[32];
-    __shared__ double sh_alpha, sh_tau;
-    __shared__ double G[QB][QB];
+    __shared__ double s_alpha, s_tau, s_v0;
+    __shared__ double G[QB][QB + 1];
+    __shared__ double Tsh[QB][QB + 1];
     const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, wid = tid >> 5, nwb = nt >> 5;
+    const int R = m - j0;                          // panel rows j0..m-1
+    // panel P (R x jb, ld R): shared memory or the matrix itself
+    double *P = use_smem ? smp : nullptr;
+    const int ldp = use_smem ? R : m;
+    if (use_smem) {
+        for (long idx = tid; idx < (long)R * jb; idx += nt) {
+            int i = (int)(idx % R), c = (int)(idx / R);
+            P[idx] = W[(long)(j0 + c) * m + j0 + i];
+        }
+    } else {
+        P = W + (long)j0 * m + j0;
+    }
+    __syncthreads();
     for (int jj = 0; jj < jb; jj++) {
-        const int j = j0 + jj;
-        double *x = W + (long)j * m;
+        double *x = P + (long)jj * ldp;           // rows jj..R-1 are the active part
         double s = 0.0;
-        for (int i = j + tid; i < m; i += nt) s = fma(x[i], x[i], s);
+        for (int i = jj + 1 + tid; i < R; i += nt) s = fma(x[i], x[i], s);
         s = block_sum(s, red);
-        const double nrm = sqrt(s);
-        double *v = V + (long)j * m;
         if (tid == 0) {
-            if (nrm == 0.0) { sh_tau = 0.0; sh_alpha = 0.0; }
+            double x0 = x[jj];
+            double nrm2 = s + x0 * x0;
+            if (nrm2 == 0.0) { s_tau = 0.0; s_alpha = 0.0; s_v0 = 0.0; }
             else {
-                double x0 = x[j];
+                double nrm = sqrt(nrm2);
                 double alpha = (x0 >= 0.0) ? -nrm : nrm;
-                sh_alpha = alpha;
-                // v^T v = (x0-alpha)^2 + (s - x0^2) = 2 nrm (nrm + |x0|)
                 double v0 = x0 - alpha;
-                sh_tau = 2.0 / (v0 * v0 + (s - x0 * x0));
-                v[j] = v0;
+                s_alpha = alpha; s_v0 = v0;
+                s_tau = 2.0 / (v0 * v0 + s);
             }
         }
         __syncthreads();
-        const double tj = sh_tau;
-        for (int i = tid; i < m; i += nt) {
-            if (i < j) v[i] = 0.0;
-            else if (i > j) v[i] = (tj == 0.0) ? 0.0 : x[i];
-        }
-        if (tid == 0 && tj == 0.0) v[j] = 0.0;
+        const double tj = s_tau;
+        if (tid == 0) { tau[j0 + jj] = tj; x[jj] = (tj == 0.0) ? x[jj] : s_v0; }   // x now holds v (rows jj..)
         __syncthreads();
-        // apply H_j to the remaining panel columns
-        for (int cc = jj + 1; cc < jb; cc++) {
-            double *y = W + (long)(j0 + cc) * m;
-            double d = 0.0;
-            if (tj != 0.0)
-                for (int i = j + tid; i < m; i += nt) d = fma(v[i], y[i], d);
-            d = block_sum(d, red);
-            const double f = tj * d;
-            if (tj != 0.0)
-                for (int i = j + tid; i < m; i += nt) y[i] = fma(-f, v[i], y[i]);
-            __syncthreads();
-        }
-        if (tid == 0) { tau[j] = tj; }
-        // column j of W becomes alpha e_j
-        for (int i = j + tid; i < m; i += nt) x[i] = (i == j) ? ((tj == 0.0) ? x[j] : sh_alpha) : 0.0;
+        // apply H_j to the remaining panel columns: one warp per column
+        if (tj != 0.0)
+            for (int cc = jj + 1 + wid; cc < jb; cc += nwb) {
+                double *y = P + (long)cc * ldp;
+                double d = 0.0;
+                for (int i = jj + lane; i < R; i += 32) d = fma(x[i], y[i], d);
+                d = warp_sum(d);
+                const double f = tj * d;
+                for (int i = jj + lane; i < R; i += 32) y[i] = fma(-f, x[i], y[i]);
+            }
         __syncthreads();
     }
-    // Gram G = V_p^T V_p (warp per entry), then T (forward, columnwise)
-    const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
-    for (int e = w; e < jb * jb; e += nw) {
+    // write V (full columns of length m) and R-part of W; x[jj] (the v0) -> alpha
+    for (long idx = tid; idx < (long)m * jb; idx += nt) {
+        int i = (int)(idx % m), c = (int)(idx / m);
+        const int j = j0 + c;
+        double vv = 0.0;
+        if (i >= j && tau[j] != 0.0) vv = P[(long)c * ldp + (i - j0)];
+        V[(long)j * m + i] = vv;
+    }
+    __syncthreads();
+    // Gram of the panel's reflectors (warp per entry) -> T
+    for (int e = wid; e < jb * jb; e += nwb) {
         int a = e / jb, c = e % jb;
         double d = 0.0;
         if (a <= c) {
             const double *va = V + (long)(j0 + a) * m, *vc = V + (long)(j0 + c) * m;
-            for (int i = j0 + lane; i < m; i += 32) d = fma(va[i], vc[i], d);
+            for (int i = j0 + a + lane; i < m; i += 32) d = fma(va[i], vc[i], d);
             d = warp_sum(d);
         }
         if (lane == 0) G[a][c] = d;
     }
+    // R part: column j0+c of W: rows < j0 unchanged, rows j0..j0+c from P (above the
+    // diagonal) with the diagonal = alpha, below = 0
     __syncthreads();
-    if (tid == 0) {
-        double T[QB][QB];
-        for (int a = 0; a < QB; a++) for (int c = 0; c < QB; c++) T[a][c] = 0.0;
+    if (tid < 32) {
+        for (int c = 0; c < QB; c++) Tsh[tid][c] = 0.0;
+    }
+    __syncthreads();
+    if (tid < 32) {
+        const int a = tid;
         for (int c = 0; c < jb; c++) {
-            double tc = tau[j0 + c];
-            T[c][c] = tc;
-            // T[0:c, c] = -tau_c T[0:c, 0:c] (V[:,0:c]^T v_c)
-            for (int a = 0; a < c; a++) {
-                double sacc = 0.0;
-                for (int l = a; l < c; l++) sacc += T[a][l] * G[l][c];
-                T[a][c] = -tc * sacc;
-            }
+            const double tc = tau[j0 + c];
+            double sacc = 0.0;
+            if (a < c)
+                for (int l = a; l < c; l++) sacc = fma(Tsh[a][l], G[l][c], sacc);
+            __syncwarp();
+            if (a < c) Tsh[a][c] = -tc * sacc;
+            if (a == c) Tsh[a][c] = tc;
+            __syncwarp();
         }
-        for (int a = 0; a < QB; a++) for (int c = 0; c < QB; c++) Tp[a + c * QB] = T[a][c];
+        for (int c = 0; c < QB; c++) Tp[a + c * QB] = Tsh[a][c];
+    }
+    for (long idx = tid; idx < (long)R * jb; idx += nt) {
+        int i = (int)(idx % R), c = (int)(idx / R);
+        const int j = j0 + c;
+        double out;
+        if (i < c) out = P[(long)c * ldp + i];
+        else if (i == c) {
+            // diagonal: alpha (recomputed as -sign(x0)||x||: stored implicitly: R_jj = v0 - ... )
+            out = 0.0;   // filled below
+        } else out = 0.0;
+        if (i != c) W[(long)j * m + j0 + i] = out;
     }
 }
+
+// diagonal entries alpha_j = -sign(x0) ||x||: recovered from v0 and tau: with
+// v0 = x0 - alpha and tau = 2/(v^T v) = 1/(||x|| (||x|| + |x0|)) -> alpha = x0 - v0.
+// The panel kernel keeps x0 implicitly; we store alpha separately instead.
 
 __global__ void set_identity_kernel(int m, int k, double *Q) {
     long tot = (long)m * k;
@@ -112,21 +147,27 @@ __global__ void set_identity_kernel(int m, int k, double *Q) {
 }
 
 // R = upper k x n part of W, then the sign fix on R rows and Q columns.
-__global__ void qr_finish_kernel(int m, int n, int k, const double *__restrict__ W, double *__restrict__ Q,
-                                 double *__restrict__ R)
+__global__ void qr_finish_kernel(int m, int n, int k, const double *__restrict__ W, const double *__restrict__ diag,
+                                 double *__restrict__ Q, double *__restrict__ R)
 {
     long tot = (long)k * n;
     for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < tot; idx += (long)gridDim.x * blockDim.x) {
         int i = (int)(idx % k), c = (int)(idx / k);
-        double sg = (W[(long)i * m + i] < 0.0) ? -1.0 : 1.0;
-        R[idx] = (i <= c) ? sg * W[(long)c * m + i] : 0.0;
+        double sg = (diag[i] < 0.0) ? -1.0 : 1.0;
+        double v = (i < c) ? W[(long)c * m + i] : (i == c ? diag[i] : 0.0);
+        R[idx] = sg * v;
     }
     long totq = (long)m * k;
     for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < totq; idx += (long)gridDim.x * blockDim.x) {
         int c = (int)(idx / m);
-        if (W[(long)c * m + c] < 0.0) Q[idx] = -Q[idx];
+        if (diag[c] < 0.0) Q[idx] = -Q[idx];
     }
 }
+
+// diag_j = alpha_j (or the untouched x0 when tau_j = 0) from V's leading entry:
+// alpha = x0 - v0 where x0 = v0 + alpha ... we recompute alpha from ||x||: the panel
+// stores ||x|| implicitly in tau: tau = 2/(v0^2 + s), v0 = x0 - alpha, alpha^2 = x0^2 + s.
+// Simplest exact route: alpha_j = -(sign v0) * ... -> keep an explicit array instead.
 
 int QrWork::alloc(int mmax_, int nmax_) {
     mmax = mmax_; nmax = nmax_;
@@ -134,23 +175,52 @@ int QrWork::alloc(int mmax_, int nmax_) {
     LYAP_CUDA_TRY(cudaMalloc(&V, sizeof(double) * (size_t)mmax * kmax));
     LYAP_CUDA_TRY(cudaMalloc(&T, sizeof(double) * (size_t)QB * QB * (kmax / QB + 1)));
     LYAP_CUDA_TRY(cudaMalloc(&W, sizeof(double) * (size_t)2 * QB * (nmax > mmax ? nmax : mmax)));
-    LYAP_CUDA_TRY(cudaMalloc(&tau, sizeof(double) * (size_t)kmax));
+    LYAP_CUDA_TRY(cudaMalloc(&tau, sizeof(double) * (size_t)2 * kmax));
     LYAP_CUDA_TRY(cudaMalloc(&Wk, sizeof(double) * (size_t)mmax * nmax));
     return LYAP_OK;
 }
 void QrWork::release() { cudaFree(V); cudaFree(T); cudaFree(W); cudaFree(tau); cudaFree(Wk); V = T = W = tau = Wk = nullptr; }
 
+// alpha_j from the reflector: v = x - alpha e1 and tau = 2/(v^T v), ||v||^2 = 2 ||x||(||x|| + |x0|)
+// -> with v0 = x0 - alpha, alpha = -sign(x0) ||x||:  v0 = x0 + sign(x0)||x||, so
+// alpha = -sign(v0) * (|v0| - |x0|) = x0 - v0.  x0 is not kept, but v^T v = 2/tau and
+// v0^2 - (v0^T v - v0^2)... -> we simply compute alpha = x0 - v0 inside the panel kernel.
+__global__ void qr_alpha_kernel(int m, int j0, int jb, const double *__restrict__ V, const double *__restrict__ tau,
+                                double *__restrict__ diag)
+{
+    // ||x||^2 = v0^2 + s where s = sum_{i>j} v_i^2 and v^T v = v0^2 + s = 2/tau -> the
+    // norm of x is sqrt(x0^2 + s); with x0 = v0 + alpha and alpha^2 = x0^2 + s:
+    //   alpha = -(v0^2 + s) / (2 v0) = -(1/tau)/v0
+    const int c = threadIdx.x;
+    if (c < jb) {
+        const int j = j0 + c;
+        const double t = tau[j];
+        diag[j] = (t == 0.0) ? 0.0 : -(1.0 / t) / V[(long)j * m + j];
+    }
+}
+
 int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, QrWork &w)
 {
     if (m <= 0 || n <= 0) return LYAP_OK;
     if (m > w.mmax || n > w.nmax) return LYAP_ERR_CAPACITY;
+    KTimer kt(KC_QR, s);
     const int k = m < n ? m : n;
     double *Wm = w.Wk;
+    double *diag = w.tau + k;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
     LYAP_CUDA_TRY(cudaMemcpyAsync(Wm, A, sizeof(double) * (size_t)m * n, cudaMemcpyDeviceToDevice, s));
     for (int j0 = 0; j0 < k; j0 += QB) {
         int jb = (k - j0 < QB) ? k - j0 : QB;
         double *Tp = w.T + (size_t)(j0 / QB) * QB * QB;
-        qr_panel_kernel<<<1, 512, 0, s>>>(m, j0, jb, Wm, w.V, w.tau, Tp);
+        const size_t smem = sizeof(double) * (size_t)(m - j0) * jb;
+        const bool use_smem = smem <= 180 * 1024;
+        qr_panel_kernel<<<1, 512, use_smem ? smem : 0, s>>>(m, j0, jb, Wm, w.V, w.tau, Tp, use_smem ? 1 : 0);
+        LYAP_TRY(launched());
+        qr_alpha_kernel<<<1, 32, 0, s>>>(m, j0, jb, w.V, w.tau, diag);
         LYAP_TRY(launched());
         int nt = n - (j0 + jb);
         if (nt > 0) {
@@ -158,10 +228,10 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
             double *Wt = Wm + (size_t)(j0 + jb) * m;
             // Y = V_p^T Wt (jb x nt)      (rows j0..m-1 suffice: V zero above)
             LYAP_TRY(dgemm_cm(s, true, false, jb, nt, m - j0, 1.0, Vp + j0, m, Wt + j0, m, 0.0, w.W, QB));
-            // Y = T^T Y  (in place via a second buffer region: use Q as scratch? no - small copy)
+            // Y2 = T^T Y
             LYAP_TRY(gemm_strided<double, double, double, double>(s, jb, nt, jb, 1.0, Tp, QB, 1, w.W, 1, QB,
                                                                   0.0, w.W + (size_t)QB * nt, 1, QB));
-            // Wt -= V_p Y
+            // Wt -= V_p Y2
             LYAP_TRY(dgemm_cm(s, false, false, m - j0, nt, jb, -1.0, Vp + j0, m, w.W + (size_t)QB * nt, QB, 1.0,
                               Wt + j0, m));
         }
@@ -182,7 +252,7 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
                           Qc + j0, m));
     }
     int tot = (int)(((long)k * n + (long)m * k + 255) / 256);
-    qr_finish_kernel<<<tot < 1024 ? tot : 1024, 256, 0, s>>>(m, n, k, Wm, Q, R);
+    qr_finish_kernel<<<tot < 1024 ? tot : 1024, 256, 0, s>>>(m, n, k, Wm, diag, Q, R);
     return launched();
 }
 

@@ -215,15 +215,26 @@ tridiag_kernel_2sync(TridArgs a)
 
 // ---------------------------------------------------------------- 2. divide and conquer
 // Leaf: dense eigendecomposition of the tridiagonal block [lo, hi) (size <= 32) by
-// cyclic Jacobi in one warp; eigenvalues ascending into lam, vectors into Q block.
-__global__ void __launch_bounds__(32)
+// parallel (round-robin) Jacobi in one CTA; eigenvalues ascending into lam, vectors
+// into the Q block.
+__device__ __forceinline__ void leaf_pair(int r, int i, int N, int &a, int &b) {
+    if (i == 0) { a = r; b = N - 1; }
+    else { a = (r + i) % (N - 1); b = (r - i + (N - 1)) % (N - 1); }
+    if (a > b) { int x = a; a = b; b = x; }
+}
+
+__global__ void __launch_bounds__(256)
 dc_leaf_kernel(int p, const int *__restrict__ bounds, const double *__restrict__ d, const double *__restrict__ e,
                double *__restrict__ lam, double *__restrict__ Q)
 {
-    __shared__ double M[32][33], V[32][33];
+    __shared__ double M[32][33], V[32][33], cs[32][2];
+    __shared__ double red[32];
+    __shared__ int any;
     const int lo = bounds[blockIdx.x], hi = bounds[blockIdx.x + 1], n = hi - lo;
-    const int t = threadIdx.x;
-    for (int r = 0; r < 32; r++) {
+    const int tid = threadIdx.x;
+    const int N = n + (n & 1), np = N / 2;
+    for (int idx = tid; idx < 32 * 32; idx += blockDim.x) {
+        int r = idx / 32, t = idx % 32;
         double mv = 0.0;
         if (t < n && r < n) {
             if (r == t) mv = d[lo + r];
@@ -233,41 +244,67 @@ dc_leaf_kernel(int p, const int *__restrict__ bounds, const double *__restrict__
         M[r][t] = mv;
         V[r][t] = (r == t) ? 1.0 : 0.0;
     }
-    __syncwarp();
-    double fro = 0.0;
-    for (int r = 0; r < n; r++) if (t < n) fro += M[r][t] * M[r][t];
-    fro = sqrt(warp_sum(fro));
-    for (int sweep = 0; sweep < 40; sweep++) {
-        double off = 0.0;
-        for (int r = 0; r < n; r++) if (t < n && r != t) off += M[r][t] * M[r][t];
-        off = sqrt(warp_sum(off));
+    __syncthreads();
+    double f2 = 0.0;
+    for (int idx = tid; idx < n * n; idx += blockDim.x) f2 += M[idx / n][idx % n] * M[idx / n][idx % n];
+    const double fro = sqrt(block_sum(f2, red));
+    for (int sweep = 0; sweep < 40 && n > 1; sweep++) {
+        double o2 = 0.0;
+        for (int idx = tid; idx < n * n; idx += blockDim.x) { int r = idx / n, t = idx % n; if (r != t) o2 += M[r][t] * M[r][t]; }
+        const double off = sqrt(block_sum(o2, red));
         if (off <= 0x1p-53 * fro || off == 0.0) break;
-        for (int pp = 0; pp < n - 1; pp++)
-            for (int q = pp + 1; q < n; q++) {
-                double apq = M[pp][q];
-                if (apq == 0.0) continue;
-                double app = M[pp][pp], aqq = M[q][q];
-                double tt = (aqq - app) / (2.0 * apq);
-                double tn = isinf(tt) ? 0.0 : ((tt >= 0.0) ? 1.0 : -1.0) / (fabs(tt) + sqrt(1.0 + tt * tt));
-                double c = 1.0 / sqrt(1.0 + tn * tn), s = tn * c;
-                __syncwarp();
-                if (t < n) {           // columns pp, q of row t
-                    double a1 = M[t][pp], a2 = M[t][q];
-                    M[t][pp] = c * a1 - s * a2; M[t][q] = s * a1 + c * a2;
+        if (tid == 0) any = 0;
+        __syncthreads();
+        for (int rr = 0; rr < N - 1; rr++) {
+            if (tid < np) {
+                int a, b;
+                leaf_pair(rr, tid, N, a, b);
+                double c = 1.0, s = 0.0;
+                if (b < n) {
+                    double apq = M[a][b];
+                    if (apq != 0.0 && fabs(apq) > 0x1p-53 * sqrt(fabs(M[a][a] * M[b][b]))) {
+                        double tt = (M[b][b] - M[a][a]) / (2.0 * apq);
+                        double tn = isinf(tt) ? 0.0 : ((tt >= 0.0) ? 1.0 : -1.0) / (fabs(tt) + sqrt(1.0 + tt * tt));
+                        c = 1.0 / sqrt(1.0 + tn * tn); s = tn * c;
+                        any = 1;
+                    }
                 }
-                __syncwarp();
-                if (t < n) {           // rows pp, q of column t
-                    double a1 = M[pp][t], a2 = M[q][t];
-                    M[pp][t] = c * a1 - s * a2; M[q][t] = s * a1 + c * a2;
-                    double v1 = V[t][pp], v2 = V[t][q];
-                    V[t][pp] = c * v1 - s * v2; V[t][q] = s * v1 + c * v2;
-                }
-                __syncwarp();
-                if (t == 0) { M[pp][q] = 0.0; M[q][pp] = 0.0; }
-                __syncwarp();
+                cs[tid][0] = c; cs[tid][1] = s;
             }
+            __syncthreads();
+            for (int q = tid; q < np * np; q += blockDim.x) {       // A <- J^T A J, 2x2 blocks
+                int P = q % np, R = q / np, a, b, a2, b2;
+                leaf_pair(rr, P, N, a, b);
+                leaf_pair(rr, R, N, a2, b2);
+                const bool bv = b < n, b2v = b2 < n;
+                double c1 = cs[P][0], s1 = cs[P][1], c2 = cs[R][0], s2 = cs[R][1];
+                double m00 = M[a][a2], m01 = b2v ? M[a][b2] : 0.0;
+                double m10 = bv ? M[b][a2] : 0.0, m11 = (bv && b2v) ? M[b][b2] : 0.0;
+                double n00 = c2 * m00 - s2 * m01, n01 = s2 * m00 + c2 * m01;
+                double n10 = c2 * m10 - s2 * m11, n11 = s2 * m10 + c2 * m11;
+                double o00 = c1 * n00 - s1 * n10, o01 = c1 * n01 - s1 * n11;
+                double o10 = s1 * n00 + c1 * n10, o11 = s1 * n01 + c1 * n11;
+                if (P == R && bv && s1 != 0.0) { o01 = 0.0; o10 = 0.0; }
+                M[a][a2] = o00;
+                if (b2v) M[a][b2] = o01;
+                if (bv) M[b][a2] = o10;
+                if (bv && b2v) M[b][b2] = o11;
+            }
+            for (int q = tid; q < n * np; q += blockDim.x) {        // V <- V J
+                int k = q % n, P = q / n, a, b;
+                leaf_pair(rr, P, N, a, b);
+                if (b >= n || cs[P][1] == 0.0) continue;
+                double c = cs[P][0], s = cs[P][1];
+                double va = V[k][a], vb = V[k][b];
+                V[k][a] = c * va - s * vb;
+                V[k][b] = s * va + c * vb;
+            }
+            __syncthreads();
+        }
+        if (!any) break;
     }
     // sort ascending (rank by comparison)
+    const int t = tid;
     if (t < n) {
         double dt = M[t][t];
         int rank = 0;
@@ -520,46 +557,26 @@ __global__ void dc_sort_kernel(int p, const MergeInfo *__restrict__ mi, const do
 }
 
 // ---------------------------------------------------------------- 3. back-transformation
-// V panel (p x jb) of reflectors j0..j0+jb-1: V[:, jj] = [0..0, 1 (row j+1), A[j+2:, j]]
-__global__ void bt_panel_kernel(int p, int j0, int jb, const double *__restrict__ A, const double *__restrict__ tau,
-                                double *__restrict__ V, double *__restrict__ Tp)
+// Compact-WY factor T (jb x jb, ld 32) of reflectors with Gram G = V^T V (ld 32):
+// T[c][c] = tau_c, T[0:c, c] = -tau_c T[0:c, 0:c] G[0:c, c]  (forward, columnwise).
+// One warp; column c is computed in parallel over its rows.
+__global__ void wy_T_kernel(int jb, const double *__restrict__ G, const double *__restrict__ tau, double *__restrict__ Tp)
 {
-    __shared__ double G[32][33];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (long idx = tid; idx < (long)p * jb; idx += nt) {
-        int i = (int)(idx % p), jj = (int)(idx / p), j = j0 + jj;
-        double v = 0.0;
-        if (i == j + 1) v = 1.0;
-        else if (i > j + 1) v = A[(long)j * p + i];
-        if (tau[j] == 0.0) v = 0.0;
-        V[idx] = v;
+    __shared__ double T[32][33];
+    const int a = threadIdx.x;
+    for (int c = 0; c < 32; c++) T[a][c] = 0.0;
+    __syncwarp();
+    for (int c = 0; c < jb; c++) {
+        const double tc = tau[c];
+        double sacc = 0.0;
+        if (a < c)
+            for (int l = a; l < c; l++) sacc = fma(T[a][l], G[l + c * 32], sacc);
+        __syncwarp();
+        if (a < c) T[a][c] = -tc * sacc;
+        if (a == c) T[a][c] = tc;
+        __syncwarp();
     }
-    __syncthreads();
-    const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
-    for (int q = w; q < jb * jb; q += nw) {
-        int a = q / jb, c = q % jb;
-        double s = 0.0;
-        if (a <= c) {
-            for (int i = lane; i < p; i += 32) s = fma(V[(long)a * p + i], V[(long)c * p + i], s);
-            s = warp_sum(s);
-        }
-        if (lane == 0) G[a][c] = s;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        double T[32][32];
-        for (int a = 0; a < 32; a++) for (int c = 0; c < 32; c++) T[a][c] = 0.0;
-        for (int c = 0; c < jb; c++) {
-            double tc = tau[j0 + c];
-            T[c][c] = tc;
-            for (int a = 0; a < c; a++) {
-                double sacc = 0.0;
-                for (int l = a; l < c; l++) sacc += T[a][l] * G[l][c];
-                T[a][c] = -tc * sacc;
-            }
-        }
-        for (int a = 0; a < 32; a++) for (int c = 0; c < 32; c++) Tp[a + c * 32] = T[a][c];
-    }
+    for (int c = 0; c < 32; c++) Tp[a + c * 32] = T[a][c];
 }
 
 // eigenvalues descending + sign normalisation (largest |component| positive, lowest index)
@@ -637,6 +654,8 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
     }
     if (prof) cudaEventRecord(pev[0], s);
     // 1. tridiagonalisation (reflectors stay in W.A until the back-transformation)
+    zero_d_kernel<<<gsz, 256, 0, s>>>((long)pp, W.R);
+    LYAP_TRY(launched());
     symmetrize_copy_kernel<<<gsz, 256, 0, s>>>(p, Ain, W.A);
     LYAP_TRY(launched());
     {
@@ -677,7 +696,7 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
     LYAP_CUDA_TRY(cudaMemcpyAsync(bounds, hb.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice, s));
     zero_d_kernel<<<gsz, 256, 0, s>>>((long)pp, W.Q);
     LYAP_TRY(launched());
-    dc_leaf_kernel<<<nl, 32, 0, s>>>(p, bounds, d, e, lam, W.Q);
+    dc_leaf_kernel<<<nl, 256, 0, s>>>(p, bounds, d, e, lam, W.Q);
     LYAP_TRY(launched());
     for (int width = 1; width < nl; width *= 2) {
         std::vector<MergeInfo> hm;
@@ -720,13 +739,16 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
     const int nref = std::max(p - 2, 0);
     for (int j0 = ((nref - 1) / 32) * 32; nref > 0 && j0 >= 0; j0 -= 32) {
         const int jb = std::min(32, nref - j0);
-        bt_panel_kernel<<<1, 512, 0, s>>>(p, j0, jb, W.R, tau, W.Qg, Tp);
+        // V = reflectors j0..j0+jb-1 as stored (zero above the unit entry), p x jb, ld p
+        const double *Vp = W.R + (size_t)j0 * p;
+        LYAP_TRY(dgemm_cm(s, true, false, jb, jb, p, 1.0, Vp, p, Vp, p, 0.0, W.Qk, 32));
+        wy_T_kernel<<<1, 32, 0, s>>>(jb, W.Qk, tau + j0, Tp);
         LYAP_TRY(launched());
-        // Wt = V^T X (jb x p) ; Wt2 = T Wt ; X -= V Wt2    (V = W.Qg, p x jb)
-        LYAP_TRY(dgemm_cm(s, true, false, jb, p, p, 1.0, W.Qg, p, W.Q, p, 0.0, W.Qk, 32));
+        // Wt = V^T X (jb x p) ; Wt2 = T Wt ; X -= V Wt2
+        LYAP_TRY(dgemm_cm(s, true, false, jb, p, p, 1.0, Vp, p, W.Q, p, 0.0, W.Qk, 32));
         LYAP_TRY(gemm_strided<double, double, double, double>(s, jb, p, jb, 1.0, Tp, 1, 32, W.Qk, 1, 32, 0.0,
                                                               W.U, 1, 32));
-        LYAP_TRY(dgemm_cm(s, false, false, p, p, jb, -1.0, W.Qg, p, W.U, 32, 1.0, W.Q, p));
+        LYAP_TRY(dgemm_cm(s, false, false, p, p, jb, -1.0, Vp, p, W.U, 32, 1.0, W.Q, p));
     }
     eigfinal_kernel<<<std::min(ceil_div((long)p * 32, 256), 1024), 256, 0, s>>>(p, lam, W.Q, w_out, V_out);
     LYAP_TRY(launched());
