@@ -184,6 +184,17 @@ int lyap_sol_upt_chol(lyap_ir_handle h, int c, const double *Z, int cp,
                       const double *Zp, int cm, const double *Zm, double eta_s,
                       double *Zn, int *r);
 
+/* Tensor-core (tcgen05, TMEM accumulator, TMA-fed) product of the 16-bit solver
+ * precisions used by the inversion update and the A_k^{-1} Z_k products
+ * (Eq. newton-lyapu1 l.1125, Alg. 3/4 line 4):
+ *   C = alpha * A * B^T + beta * C
+ *   A  device, M x K row-major (ld lda), B device, N x K row-major (ld ldb),
+ *   C  device, M x N row-major (ld ldc); all of type prec (LYAP_BF16/LYAP_FP16),
+ *   fp32 accumulation.  lda, ldb multiples of 8; A, B 16-byte aligned.
+ * Errors: ARG (precision / alignment), CUDA. */
+int lyap_tc_gemm(int prec, int M, int N, int K, float alpha, const void *A, long lda,
+                 const void *B, long ldb, float beta, void *C, long ldc, void *stream);
+
 /* Number of this library's kernel launches since load (a counter the bench
  * reports as gpu_launches). */
 int64_t lyap_launch_count(void);

@@ -62,7 +62,7 @@ SYMBOLS = ["lyap_ir_default_options", "lyap_ir_create", "lyap_ir_destroy", "lyap
            "lyap_ir_solve_host", "lyap_invert", "lyap_newton_aseq", "lyap_newton_get_inverse",
            "lyap_newton_z", "lyap_qr", "lyap_syev", "lyap_rank_trunc_chol", "lyap_rank_trunc_ldlt",
            "lyap_res_fac_ldlt", "lyap_res_fac_chol", "lyap_sol_upt_ldlt", "lyap_sol_upt_chol",
-           "lyap_launch_count", "lyap_kernel_timing", "lyap_kernel_stats"]
+           "lyap_launch_count", "lyap_kernel_timing", "lyap_kernel_stats", "lyap_tc_gemm"]
 
 KERNEL_CLASSES = {"gje_update": 0, "gje_panel": 1, "zside_gemm": 2, "jacobi": 3, "qr": 4,
                   "resid_gemm": 5, "newton_update": 6}
@@ -104,6 +104,9 @@ def lib():
         L.lyap_sol_upt_ldlt.argtypes = [vp, C.c_int, dp, dp, C.c_int, dp, dp, C.c_double, dp, dp, ip]
         L.lyap_sol_upt_chol.argtypes = [vp, C.c_int, dp, C.c_int, dp, C.c_int, dp, C.c_double, dp, ip]
         L.lyap_launch_count.restype = C.c_int64
+        L.lyap_tc_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, vp, C.c_long, vp, C.c_long,
+                                   C.c_float, vp, C.c_long, vp]
+        L.lyap_tc_gemm.restype = C.c_int
         L.lyap_kernel_timing.argtypes = [C.c_int]
         L.lyap_kernel_stats.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         for s in SYMBOLS:
@@ -311,6 +314,18 @@ def invert(A, ipiv=None):
     dt = {torch.float64: FP64, torch.float32: FP32, torch.float16: FP16, torch.bfloat16: BF16}[A.dtype]
     _check(lib().lyap_invert(A.shape[0], dt, _ptr(A), _ptr(ipiv), _stream()), "lyap_invert")
     return A
+
+
+def tc_gemm(A, B, C, alpha=1.0, beta=0.0):
+    """C = alpha A B^T + beta C on the tcgen05 tensor cores (A: M x K, B: N x K, C: M x N,
+    contiguous bf16/fp16 CUDA tensors of one dtype)."""
+    import torch
+    prec = {torch.bfloat16: BF16, torch.float16: FP16}[A.dtype]
+    M, K = A.shape
+    N = B.shape[0]
+    _check(lib().lyap_tc_gemm(prec, M, N, K, alpha, _ptr(A), K, _ptr(B), K, beta, _ptr(C), N, _stream()),
+           "lyap_tc_gemm")
+    return C
 
 
 def qr(At):

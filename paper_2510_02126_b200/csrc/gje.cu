@@ -213,7 +213,7 @@ __global__ void gje_prep_kernel(int n, int k, int b, T *__restrict__ A, const in
             const bool panel_col = (c >= k && c < k + b);
             if (in_block) {
                 T v = (slot >= 0) ? tmp[(long)slot * n + c] : A[i * n + c];
-                B[(long)local * n + c] = panel_col ? ((c - k == local) ? one : zero) : v;
+                B[(long)c * b + local] = panel_col ? ((c - k == local) ? one : zero) : v;   // Bt: n x b
                 A[i * n + c] = zero;
             } else if (slot >= 0) {
                 A[i * n + c] = panel_col ? zero : tmp[(long)slot * n + c];
@@ -316,7 +316,12 @@ template <typename T>
 int gemm_update(cudaStream_t s, int n, int b, const T *X, const T *B, T *A)
 {
     using Acc = typename Prec<T>::acc;
-    return gemm_strided<T, T, T, Acc>(s, n, n, b, Acc(1), X, b, 1, B, n, 1, Acc(1), A, n, 1);
+    // B holds the pivot rows transposed (Bt, n x b row-major): A += X Bt^T
+    if constexpr (std::is_same<T, __half>::value || std::is_same<T, __nv_bfloat16>::value) {
+        if (!use_simt_gemm() && b % 8 == 0)     // TMA rows must be 16-byte multiples
+            return tc_gemm(s, Prec<T>::code, n, n, b, 1.0f, X, b, B, b, 1.0f, A, n, 0);
+    }
+    return gemm_strided<T, T, T, Acc>(s, n, n, b, Acc(1), X, b, 1, B, 1, b, Acc(1), A, n, 1);
 }
 template int gemm_update<double>(cudaStream_t, int, int, const double *, const double *, double *);
 template int gemm_update<float>(cudaStream_t, int, int, const float *, const float *, float *);

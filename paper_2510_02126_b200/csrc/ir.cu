@@ -62,6 +62,7 @@ struct lyap_ir_ctx {
     double *hA = nullptr, *hL = nullptr, *hS = nullptr, *hZ = nullptr, *hY = nullptr;
     cudaEvent_t ev[8];
     double t_newton = 0, t_res = 0, t_upd = 0;
+    bool zorth = false;        // leading factor columns are orthonormal (set by the IR loop)
 };
 
 namespace {
@@ -92,6 +93,9 @@ int sync_read(lyap_ir_ctx *h, void *dst, const void *src, size_t bytes) {
 // C (n x c, col-major) = Ainv (n x n row-major, u_s) * Z (n x c, col-major, u_s)
 int zside_gemm(lyap_ir_ctx *h, const void *Ainv, const void *Z, void *Out, int c) {
     const int n = h->n;
+    if ((h->us == LYAP_BF16 || h->us == LYAP_FP16) && !use_simt_gemm() && n % 8 == 0)
+        // Out (n x c, column-major) = Ainv (n x n, row-major = K-major) * Z, Z^T rows K-major
+        return tc_gemm(h->s, h->us, n, c, n, 1.0f, Ainv, n, Z, n, 0.0f, Out, n, 1);
     switch (h->us) {
         case LYAP_FP64:
             return gemm_strided<double, double, double, double>(h->s, n, c, n, 1.0, (const double *)Ainv, n, 1,
@@ -259,6 +263,43 @@ int build_F(lyap_ir_ctx *h, const double *A, const double *L, int m, int c, cons
 
 // Fragment 3 (ldlt, Y != null, S != null) / Fragment 1 (Y == null).
 // Outputs: ldlt: Ld (n x r), Sd (r x r, ld r) ; chol: Ld = L+ (n x rp), Lm = L- (n x rm)
+// Thin QR of h->F (n x p) into h->U (n x k), h->Tm (k x p).  When the leading c
+// columns are known to be orthonormal (Z = V Theta_t from a previous solution
+// update), the QR is [Z, Q2] with R = [[I, Rz], [0, R2]]: the remaining columns are
+// projected out of span(Z) twice (block classical Gram-Schmidt with
+// reorthogonalisation) and only those are Householder-factorised.  The thin QR
+// with non-negative diag(R) is unique, so this equals the Householder result up
+// to rounding.
+int thin_qr_F(lyap_ir_ctx *h, int p, int c_orth) {
+    const int n = h->n;
+    cudaStream_t s = h->s;
+    const int c = c_orth, q = p - c;
+    // fast path only with ample room (p <= n/2) and a well-conditioned remainder
+    if (!h->zorth || c <= 0 || q <= 0 || 2 * p > n) return qr_f64(s, n, p, h->F, h->U, h->Tm, h->qr);
+    const double *Z = h->F;
+    double *B = h->F + (size_t)n * c;
+    double *X1 = h->TN, *X2 = h->Hm, *R2 = h->Vs;
+    LYAP_TRY(nk_copy_block(s, n, q, B, n, h->Zd2, n, 1.0));   // keep B for the fallback
+    LYAP_TRY(dgemm_cm(s, true, false, c, q, n, 1.0, Z, n, B, n, 0.0, X1, c));
+    LYAP_TRY(dgemm_cm(s, false, false, n, q, c, -1.0, Z, n, X1, c, 1.0, B, n));
+    LYAP_TRY(dgemm_cm(s, true, false, c, q, n, 1.0, Z, n, B, n, 0.0, X2, c));
+    LYAP_TRY(dgemm_cm(s, false, false, n, q, c, -1.0, Z, n, X2, c, 1.0, B, n));
+    LYAP_TRY(nk_axpy(s, (long)c * q, 1.0, X2, X1));          // Rz = X1 + X2
+    const int k2 = std::min(n - c, q);
+    LYAP_TRY(qr_f64(s, n, q, B, h->U + (size_t)n * c, R2, h->qr));
+    // |diag(R2)| range: a near-zero pivot would leave an arbitrary (non-orthogonal to Z)
+    // Householder completion column -> fall back to the full Householder QR
+    LYAP_TRY(nk_diag_range(s, k2, R2, k2, h->scal + SC_TR));
+    LYAP_TRY(sync_read(h, h->hscal, h->scal, sizeof(double) * SC_COUNT));
+    const double dmin = h->hscal[SC_TR], dmax = h->hscal[SC_TR + 1];
+    if (!(dmin >= 1e-6 * dmax)) {
+        LYAP_TRY(nk_copy_block(s, n, q, h->Zd2, n, B, n, 1.0));
+        return qr_f64(s, n, p, h->F, h->U, h->Tm, h->qr);
+    }
+    LYAP_TRY(nk_copy_block(s, n, c, Z, n, h->U, n, 1.0));
+    return nk_assemble_T(s, c, q, k2, X1, R2, h->Tm);
+}
+
 int res_fac(lyap_ir_ctx *h, const double *A, const double *L, int m, const double *S, int c, const double *Z,
             const double *Y, int ldy, double eta_r, double *Ld, double *Sd, int *r, double *Lm, int *rm,
             double *resF) {
@@ -268,7 +309,7 @@ int res_fac(lyap_ir_ctx *h, const double *A, const double *L, int m, const doubl
     if (p > h->PW) return cap_fail(__LINE__, p, h->PW);
     const int k = std::min(n, p);
     LYAP_TRY(build_F(h, A, L, m, c, Z));
-    LYAP_TRY(qr_f64(s, n, p, h->F, h->U, h->Tm, h->qr));
+    LYAP_TRY(thin_qr_F(h, p, c));
     LYAP_TRY(nk_build_N(s, c, m, Y, ldy, Y ? S : nullptr, h->Nm));
     LYAP_TRY(dgemm_cm(s, false, false, k, p, p, 1.0, h->Tm, k, h->Nm, p, 0.0, h->TN, k));
     LYAP_TRY(dgemm_cm(s, false, true, k, k, p, 1.0, h->TN, k, h->Tm, k, 0.0, h->Hm, k));
@@ -315,7 +356,7 @@ int sol_upt(lyap_ir_ctx *h, int c, const double *Z, const double *Y, int ldy, in
     LYAP_TRY(nk_copy_block(s, n, c, Z, n, h->F, n, 1.0));
     LYAP_TRY(nk_copy_block(s, n, cd, Zd, n, h->F + (size_t)n * c, n, 1.0));
     if (cm > 0) LYAP_TRY(nk_copy_block(s, n, cm, Zm, n, h->F + (size_t)n * (c + cd), n, 1.0));
-    LYAP_TRY(qr_f64(s, n, p, h->F, h->U, h->Tm, h->qr));
+    LYAP_TRY(thin_qr_F(h, p, c));
     if (Y) LYAP_TRY(nk_build_blkdiag(s, c, cd, Y, ldy, Yd, ldyd, 0, h->Nm));
     else LYAP_TRY(nk_build_blkdiag(s, c + cd, cm, nullptr, 0, nullptr, 0, 0, h->Nm));
     LYAP_TRY(dgemm_cm(s, false, false, k, p, p, 1.0, h->Tm, k, h->Nm, p, 0.0, h->TN, k));
@@ -400,6 +441,7 @@ int ir_solve(lyap_ir_ctx *h, const double *A, const double *L, int m, const doub
         LYAP_CUDA_TRY(cudaEventRecord(h->ev[2], s));
         double resF = 0.0;
         int r = 0, rmm = 0;
+        h->zorth = (i >= 2);       // Z_i = V_{i-1} Theta_t has orthonormal columns after an update
         LYAP_TRY(res_fac(h, A, L, m, S, c, h->Zsol[cur], ldlt ? h->Ysol[cur] : nullptr, h->PW, h->opt.eta_r,
                          h->Ld, h->Sd, &r, h->Lm, &rmm, &resF));
         double nX2 = 0;
@@ -455,6 +497,7 @@ int ir_solve(lyap_ir_ctx *h, const double *A, const double *L, int m, const doub
             fprintf(stderr, "lyap: step %d rel=%.3e c=%d r=%d rm=%d cd=%d cm=%d -> %d\n", i, rel, c, r, rmm, cd,
                     cm, cn);
     }
+    h->zorth = false;
     LYAP_CUDA_TRY(cudaEventRecord(h->ev[7], s));
     LYAP_CUDA_TRY(cudaEventSynchronize(h->ev[7]));
     if (c > h->cmax) return cap_fail(__LINE__, c, h->cmax);

@@ -17,6 +17,15 @@ struct GjeWork {
 };
 
 int gje_invert(cudaStream_t s, int n, int prec, void *A, GjeWork &w);
+// LYAP_GEMM=simt routes the 16-bit products through the SIMT kernel (cross-checking)
+inline bool use_simt_gemm() {
+    static int v = -1;
+    if (v < 0) { const char *e = getenv("LYAP_GEMM"); v = (e && e[0] == 's') ? 1 : 0; }
+    return v == 1;
+}
+// tcgen05 GEMM (tc_gemm.cu): C = alpha A B^T + beta C, 16-bit A (M x K), B (N x K) row-major
+int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const void *A, long lda, const void *B,
+            long ldb, float beta, void *C, long ldc, int colmajor);
 int col_gather(cudaStream_t s, int n, int prec, const void *G, const int *invperm, void *out);
 template <typename T> int gemm_update(cudaStream_t s, int n, int b, const T *X, const T *B, T *A);
 

@@ -520,6 +520,60 @@ int nk_sumsq(cudaStream_t s, long len, const double *x, double *out)
     return launched();
 }
 
+__global__ void __launch_bounds__(1024)
+diag_range_kernel(int k, const double *__restrict__ R, int ldr, double *__restrict__ out)
+{
+    __shared__ double red[32];
+    double mx = 0.0, mn = INFINITY;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        double v = fabs(R[i + (long)i * ldr]);
+        mx = fmax(mx, v);
+        mn = fmin(mn, v);
+    }
+    mx = block_max(mx, red);
+    mn = -block_max(-mn, red);
+    if (threadIdx.x == 0) { out[0] = mn; out[1] = mx; }
+}
+int nk_diag_range(cudaStream_t s, int k, const double *R, int ldr, double *out)
+{
+    diag_range_kernel<<<1, 1024, 0, s>>>(k, R, ldr, out);
+    return launched();
+}
+
+__global__ void axpy_kernel(long len, double a, const double *__restrict__ x, double *__restrict__ y)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < len; i += (long)gridDim.x * blockDim.x)
+        y[i] = fma(a, x[i], y[i]);
+}
+int nk_axpy(cudaStream_t s, long len, double a, const double *x, double *y)
+{
+    if (len <= 0) return LYAP_OK;
+    axpy_kernel<<<grid_for(len), 256, 0, s>>>(len, a, x, y);
+    return launched();
+}
+
+// T (k x p, ld k) = [[I_c, Rz (c x q)], [0, R2 (k2 x q)]], k = c + k2, p = c + q
+__global__ void assemble_T_kernel(int c, int q, int k2, const double *__restrict__ Rz, const double *__restrict__ R2,
+                                  double *__restrict__ T)
+{
+    const int k = c + k2, p = c + q;
+    long tot = (long)k * p;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        int i = (int)(e % k), j = (int)(e / k);
+        double v = 0.0;
+        if (j < c) v = (i == j) ? 1.0 : 0.0;
+        else if (i < c) v = Rz[i + (long)(j - c) * c];
+        else v = R2[(i - c) + (long)(j - c) * k2];
+        T[e] = v;
+    }
+}
+int nk_assemble_T(cudaStream_t s, int c, int q, int k2, const double *Rz, const double *R2, double *T)
+{
+    long tot = (long)(c + k2) * (c + q);
+    assemble_T_kernel<<<grid_for(tot), 256, 0, s>>>(c, q, k2, Rz, R2, T);
+    return launched();
+}
+
 __global__ void roll_kernel(double *scal) { scal[SC_NA2] = scal[SC_RED + 1]; scal[SC_MAXA] = scal[SC_RED + 3]; }
 int nk_roll(cudaStream_t s, double *scal)
 {

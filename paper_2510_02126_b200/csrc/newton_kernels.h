@@ -44,5 +44,8 @@ int nk_build_blkdiag(cudaStream_t s, int c, int cd, const double *Y, int ldy, co
                      double *U);
 int nk_trace_prod(cudaStream_t s, int k, const double *P, double *out);
 int nk_sumsq(cudaStream_t s, long len, const double *x, double *out);
+int nk_diag_range(cudaStream_t s, int k, const double *R, int ldr, double *out);
+int nk_axpy(cudaStream_t s, long len, double a, const double *x, double *y);
+int nk_assemble_T(cudaStream_t s, int c, int q, int k2, const double *Rz, const double *R2, double *T);
 
 }  // namespace lyap

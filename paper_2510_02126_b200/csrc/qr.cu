@@ -12,6 +12,7 @@
 //   Q = H_0 ... H_{k-1} [I_k; 0] accumulated backwards the same way.
 // The sign convention diag(R) >= 0 makes the factorization unique for full
 // column rank, so it matches any other Householder QR up to rounding.
+#include <vector>
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "lyap_internal.h"
@@ -173,7 +174,7 @@ int QrWork::alloc(int mmax_, int nmax_) {
     mmax = mmax_; nmax = nmax_;
     int kmax = mmax < nmax ? mmax : nmax;
     LYAP_CUDA_TRY(cudaMalloc(&V, sizeof(double) * (size_t)mmax * kmax));
-    LYAP_CUDA_TRY(cudaMalloc(&T, sizeof(double) * (size_t)QB * QB * (kmax / QB + 1)));
+    LYAP_CUDA_TRY(cudaMalloc(&T, sizeof(double) * (size_t)QB * QB * (kmax / 8 + 2)));
     LYAP_CUDA_TRY(cudaMalloc(&W, sizeof(double) * (size_t)2 * QB * (nmax > mmax ? nmax : mmax)));
     LYAP_CUDA_TRY(cudaMalloc(&tau, sizeof(double) * (size_t)2 * kmax));
     LYAP_CUDA_TRY(cudaMalloc(&Wk, sizeof(double) * (size_t)mmax * nmax));
@@ -213,11 +214,20 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
         attr = true;
     }
     LYAP_CUDA_TRY(cudaMemcpyAsync(Wm, A, sizeof(double) * (size_t)m * n, cudaMemcpyDeviceToDevice, s));
-    for (int j0 = 0; j0 < k; j0 += QB) {
-        int jb = (k - j0 < QB) ? k - j0 : QB;
-        double *Tp = w.T + (size_t)(j0 / QB) * QB * QB;
+    // panel widths: 32, or 16/8 while the panel would not fit in shared memory
+    std::vector<int> starts;
+    for (int j0 = 0, jb; j0 < k; j0 += jb) {
+        jb = QB;
+        while (jb > 8 && sizeof(double) * (size_t)(m - j0) * jb > 200 * 1024) jb /= 2;
+        jb = std::min(jb, k - j0);
+        starts.push_back(j0);
+    }
+    starts.push_back(k);
+    for (size_t pi = 0; pi + 1 < starts.size(); pi++) {
+        const int j0 = starts[pi], jb = starts[pi + 1] - j0;
+        double *Tp = w.T + pi * QB * QB;
         const size_t smem = sizeof(double) * (size_t)(m - j0) * jb;
-        const bool use_smem = smem <= 180 * 1024;
+        const bool use_smem = smem <= 200 * 1024;
         qr_panel_kernel<<<1, 512, use_smem ? smem : 0, s>>>(m, j0, jb, Wm, w.V, w.tau, Tp, use_smem ? 1 : 0);
         LYAP_TRY(launched());
         qr_alpha_kernel<<<1, 32, 0, s>>>(m, j0, jb, w.V, w.tau, diag);
@@ -239,9 +249,9 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
     // Q = H_0 ... H_{k-1} [I; 0]
     set_identity_kernel<<<ceil_div((long)m * k, 256) < 1024 ? ceil_div((long)m * k, 256) : 1024, 256, 0, s>>>(m, k, Q);
     LYAP_TRY(launched());
-    for (int j0 = ((k - 1) / QB) * QB; j0 >= 0; j0 -= QB) {
-        int jb = (k - j0 < QB) ? k - j0 : QB;
-        const double *Tp = w.T + (size_t)(j0 / QB) * QB * QB;
+    for (int pi = (int)starts.size() - 2; pi >= 0; pi--) {
+        const int j0 = starts[pi], jb = starts[pi + 1] - j0;
+        const double *Tp = w.T + (size_t)pi * QB * QB;
         const double *Vp = w.V + (size_t)j0 * m;
         int nc = k - j0;               // columns j0..k-1 of Q are affected
         double *Qc = Q + (size_t)j0 * m;

@@ -136,6 +136,96 @@ tridiag_kernel(TridArgs a)
     if (blockIdx.x == 0 && threadIdx.x == 0) a.d[p - 1] = A[(long)(p - 1) * p + p - 1];
 }
 
+// Register-resident variant for p <= 1024: warp g owns column g for the whole
+// reduction and keeps it in registers (lane holds rows lane + 32u), so the trailing
+// matrix never leaves the register file; per step only P (p doubles) and the owner's
+// copy of column j+2 (published for the next step's reflector) go through L2.
+template <int CH>
+__global__ void __launch_bounds__(256)
+tridiag_reg_kernel(TridArgs a)
+{
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sm[];
+    const int p = a.p;
+    double *v = sm, *vn = sm + p, *w = sm + 2 * p, *c = sm + 3 * p;
+    __shared__ double red[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int g = blockIdx.x * nwb + wid;          // owned column (if < p)
+    const bool owner = g < p;
+    double *A = a.A;
+    double col[CH];
+#pragma unroll
+    for (int u = 0; u < CH; u++) {
+        int i = lane + 32 * u;
+        col[u] = (owner && i < p) ? A[(long)g * p + i] : 0.0;
+    }
+    double tau, beta;
+    make_reflector(A + 1, p - 1, v, red, tau, beta);
+    if (owner && g >= 1) {
+        double s = 0.0;
+#pragma unroll
+        for (int u = 0; u < CH; u++) { int i = lane + 32 * u; if (i >= 1 && i < p) s = fma(col[u], v[i - 1], s); }
+        s = warp_sum(s);
+        if (lane == 0) a.P[g] = tau * s;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.d[0] = A[0];
+    grid.sync();
+    for (int j = 0; j + 2 < p; j++) {
+        const int L = p - j - 1, r0 = j + 1;
+        double k = 0.0;
+        for (int i = threadIdx.x; i < L; i += blockDim.x) { double t = a.P[r0 + i]; w[i] = t; k = fma(t, v[i], k); }
+        k = 0.5 * tau * block_sum(k, red);
+        for (int i = threadIdx.x; i < L; i += blockDim.x) w[i] = fma(-k, v[i], w[i]);
+        __syncthreads();
+        // column j+1 as published by its owner (state after step j-1), updated privately
+        const double *cj = A + (long)r0 * p + r0;
+        for (int i = threadIdx.x; i < L; i += blockDim.x) c[i] = cj[i] - v[i] * w[0] - w[i] * v[0];
+        __syncthreads();
+        double taun = 0.0, betan = 0.0;
+        const bool more = (j + 3 < p);
+        if (more) make_reflector(c + 1, L - 1, vn, red, taun, betan);
+        if (blockIdx.x == 0) {
+            for (int i = threadIdx.x; i < L; i += blockDim.x) a.R[(long)j * p + r0 + i] = v[i];
+            if (threadIdx.x == 0) {
+                a.e[j] = beta; a.tau[j] = tau; a.d[j + 1] = c[0];
+                if (!more) { a.e[j + 1] = c[1]; a.tau[j + 1] = 0.0; }
+            }
+        }
+        if (owner && g >= r0 + 1) {
+            const double vg = v[g - r0], wg = w[g - r0];
+            double s = 0.0;
+#pragma unroll
+            for (int u = 0; u < CH; u++) {
+                const int i = lane + 32 * u;
+                if (i >= r0 + 1 && i < p) {
+                    const double x = col[u] - v[i - r0] * wg - w[i - r0] * vg;
+                    col[u] = x;
+                    if (more) s = fma(x, vn[i - r0 - 1], s);
+                }
+            }
+            if (more) {
+                s = warp_sum(s);
+                if (lane == 0) a.P[g] = taun * s;
+            }
+            if (g == r0 + 1) {                  // publish column j+2 for the next step
+#pragma unroll
+                for (int u = 0; u < CH; u++) {
+                    const int i = lane + 32 * u;
+                    if (i >= r0 + 1 && i < p) A[(long)g * p + i] = col[u];
+                }
+            }
+            if (g == p - 1 && !more && lane == (p - 1) % 32) {
+#pragma unroll
+                for (int u = 0; u < CH; u++) if (lane + 32 * u == p - 1) a.d[p - 1] = col[u];
+            }
+        }
+        grid.sync();
+        for (int i = threadIdx.x; i < L - 1; i += blockDim.x) v[i] = vn[i];
+        tau = taun; beta = betan;
+        __syncthreads();
+    }
+}
+
 // (previous two-barrier version kept for reference in the git history)
 __global__ void __launch_bounds__(256)
 tridiag_kernel_2sync(TridArgs a)
@@ -670,10 +760,24 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tridiag_kernel, 256, smem);
             max_blocks = nsm * std::max(1, std::min(per, 1));
         }
-        int grid = std::min(max_blocks, std::max(1, p / 4));
         TridArgs ta{p, W.A, W.R, d, e, tau, P};
         void *args[] = {&ta};
-        LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)tridiag_kernel, dim3(grid), dim3(256), args, smem, s));
+        const int need = ceil_div(p, 8);             // one warp per column
+        if (p >= 3 && p <= 1024 && need <= max_blocks) {
+            static bool attr2 = false;
+            if (!attr2) {
+                cudaFuncSetAttribute(tridiag_reg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                cudaFuncSetAttribute(tridiag_reg_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                cudaFuncSetAttribute(tridiag_reg_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                attr2 = true;
+            }
+            void *fn = (p <= 256) ? (void *)tridiag_reg_kernel<8>
+                     : (p <= 512) ? (void *)tridiag_reg_kernel<16> : (void *)tridiag_reg_kernel<32>;
+            LYAP_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(need), dim3(256), args, smem, s));
+        } else {
+            int grid = std::min(max_blocks, std::max(1, p / 4));
+            LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)tridiag_kernel, dim3(grid), dim3(256), args, smem, s));
+        }
         LYAP_TRY(launched());
     }
     if (prof) cudaEventRecord(pev[1], s);

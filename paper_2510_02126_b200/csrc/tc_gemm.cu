@@ -1,0 +1,233 @@
+// tc_gemm.cu -- 5th-generation tensor-core GEMM for the 16-bit solver precisions:
+//     C = alpha * A * B^T + beta * C,  A (M x K) and B (N x K) row-major ("K-major"),
+//     bf16 or fp16 operands, fp32 accumulation in TMEM, C in the same 16-bit type
+//     (row-major or column-major output).
+// Used for the Gauss-Jordan rank-b update of the inversion (Eq. newton-lyapu1,
+// A_{k-1}^{-1}) and for the Z-side products A_{k-1}^{-1} Z_{k-1} (Alg. 3/4 line 4).
+//
+// One CTA per 128 x 128 output tile, 4 warps:
+//   warp 0 (one elected lane)  TMA producer: 64-wide K blocks of A and B into a
+//                              4-stage shared-memory ring (128B swizzle), mbarrier
+//                              full/empty pipeline;
+//   warp 1 (one elected lane)  issues tcgen05.mma.cta_group::1.kind::f16 (M=128,
+//                              N=128, K=16) into a 128-column fp32 TMEM accumulator,
+//                              tcgen05.commit releases each smem stage;
+//   warps 0-3                  epilogue: tcgen05.ld 32x32b (each thread one row),
+//                              alpha/beta blend with C, 16-bit store.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include "common.cuh"
+#include "lyap_internal.h"
+
+namespace lyap {
+
+namespace tc {
+constexpr int BM = 128, BN = 128, BK = 64, STAGES = 4;
+constexpr int A_STAGE = BM * BK * 2, B_STAGE = BN * BK * 2;          // bytes
+constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) + 1024 + 256;     // + alignment + barriers
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" :: "r"(smem_u32(b)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        :: "r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
+}
+// K-major, 128B-swizzled canonical layout: 8-row x 128-byte atoms, atoms 1024 B apart.
+__device__ __forceinline__ uint64_t smem_desc(const void *p) {
+    uint64_t a = smem_u32(p);
+    return ((a & 0x3FFFFull) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" :: "r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, float *v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; i++) v[i] = __uint_as_float(r[i]);
+}
+}  // namespace tc
+
+template <typename T>
+__global__ void __launch_bounds__(128, 1)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               int M, int N, int K, float alpha, float beta, T *__restrict__ C, long ldc, int colmajor)
+{
+    using namespace tc;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *base = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char *sA = base;
+    unsigned char *sB = base + STAGES * A_STAGE;
+    uint64_t *full = (uint64_t *)(sB + STAGES * B_STAGE);
+    uint64_t *empty = full + STAGES;
+    uint64_t *done = empty + STAGES;
+    uint32_t *tmem_slot = (uint32_t *)(done + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int nk = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        tc::mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" :: "l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" :: "l"(&tmB) : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(tc::smem_u32(tmem_slot)), "r"(BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer
+        for (int kb = 0; kb < nk; kb++) {
+            const int s = kb % STAGES;
+            if (kb >= STAGES) tc::mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+            tc::mbar_expect_tx(&full[s], A_STAGE + B_STAGE);
+            tc::tma_load_2d(sA + s * A_STAGE, &tmA, &full[s], kb * BK, m0);
+            tc::tma_load_2d(sB + s * B_STAGE, &tmB, &full[s], kb * BK, n0);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer
+        const uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+        const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
+                               ((uint32_t)(BM >> 4) << 24);
+        for (int kb = 0; kb < nk; kb++) {
+            const int s = kb % STAGES;
+            tc::mbar_wait(&full[s], (kb / STAGES) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint64_t da = tc::smem_desc(sA + s * A_STAGE), db = tc::smem_desc(sB + s * B_STAGE);
+#pragma unroll
+            for (int k = 0; k < BK / 16; k++)   // +32 bytes along K = +2 in the start-address field
+                tc::mma_f16(tmem, da + 2 * k, db + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(done);
+    }
+    // ---------------- epilogue (all 4 warps): thread = one accumulator row
+    tc::mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int row = m0 + warp * 32 + lane;
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+        if (row < M) {
+#pragma unroll
+            for (int i = 0; i < 16; i++) {
+                const int col = n0 + c0 + i;
+                if (col < N) {
+                    T *cp = colmajor ? C + (long)col * ldc + row : C + (long)row * ldc + col;
+                    float r = alpha * v[i];
+                    if (beta != 0.f) r = fmaf(beta, to_f<T>(*cp), r);
+                    *cp = from_f<T>(r);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(BN));
+}
+
+// ---------------------------------------------------------------- host side
+namespace {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    }
+    return fn;
+}
+// rows x cols row-major 16-bit matrix with leading dimension ld (elements); box = 64 x box_rows
+int make_map(CUtensorMap *m, const void *ptr, int prec, long rows, long cols, long ld, int box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return LYAP_ERR_CUDA;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, prec == LYAP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                    const_cast<void *>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? LYAP_OK : LYAP_ERR_ARG;
+}
+}  // namespace
+
+// C = alpha * A (M x K, ld lda) * B^T (B: N x K, ld ldb) + beta * C  (C ld ldc, row- or column-major)
+int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const void *A, long lda, const void *B,
+            long ldb, float beta, void *C, long ldc, int colmajor)
+{
+    if (M <= 0 || N <= 0 || K <= 0) return LYAP_OK;
+    if (prec != LYAP_BF16 && prec != LYAP_FP16) return LYAP_ERR_ARG;
+    if ((lda * 2) % 16 || (ldb * 2) % 16 || ((uintptr_t)A % 16) || ((uintptr_t)B % 16)) return LYAP_ERR_ARG;
+    CUtensorMap ma, mb;
+    LYAP_TRY(make_map(&ma, A, prec, M, K, lda, tc::BM));
+    LYAP_TRY(make_map(&mb, B, prec, N, K, ldb, tc::BN));
+    dim3 grid(ceil_div(N, tc::BN), ceil_div(M, tc::BM));
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tc_gemm_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM);
+        cudaFuncSetAttribute(tc_gemm_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM);
+        attr = true;
+    }
+    if (prec == LYAP_BF16)
+        tc_gemm_kernel<__nv_bfloat16><<<grid, 128, tc::SMEM, s>>>(ma, mb, M, N, K, alpha, beta, (__nv_bfloat16 *)C,
+                                                                   ldc, colmajor);
+    else
+        tc_gemm_kernel<__half><<<grid, 128, tc::SMEM, s>>>(ma, mb, M, N, K, alpha, beta, (__half *)C, ldc, colmajor);
+    return launched();
+}
+
+}  // namespace lyap
+
+// standalone entry for tests: C = alpha A B^T + beta C (row-major C, 16-bit types)
+extern "C" int lyap_tc_gemm(int prec, int M, int N, int K, float alpha, const void *A, long lda, const void *B,
+                            long ldb, float beta, void *C, long ldc, void *stream)
+{
+    int rc = lyap::tc_gemm((cudaStream_t)stream, prec, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
+    if (rc == LYAP_OK && cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) rc = LYAP_ERR_CUDA;
+    return rc;
+}
