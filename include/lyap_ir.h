@@ -208,6 +208,10 @@ int64_t lyap_launch_count(void);
  * lyap_kernel_timing call. */
 int lyap_kernel_timing(int cls);
 int lyap_kernel_stats(double *ms, int64_t *launches);
+/* Algorithmic flops and bytes of the launches timed since lyap_kernel_timing
+ * (classes 7 fp64 DMMA GEMM, 8 tcgen05 GEMM, 9 Householder panel, 10
+ * tridiagonalisation report them). */
+int lyap_kernel_work(double *flops, double *bytes);
 
 #ifdef __cplusplus
 }

@@ -62,10 +62,11 @@ SYMBOLS = ["lyap_ir_default_options", "lyap_ir_create", "lyap_ir_destroy", "lyap
            "lyap_ir_solve_host", "lyap_invert", "lyap_newton_aseq", "lyap_newton_get_inverse",
            "lyap_newton_z", "lyap_qr", "lyap_syev", "lyap_rank_trunc_chol", "lyap_rank_trunc_ldlt",
            "lyap_res_fac_ldlt", "lyap_res_fac_chol", "lyap_sol_upt_ldlt", "lyap_sol_upt_chol",
-           "lyap_launch_count", "lyap_kernel_timing", "lyap_kernel_stats", "lyap_tc_gemm"]
+           "lyap_launch_count", "lyap_kernel_timing", "lyap_kernel_stats", "lyap_kernel_work", "lyap_tc_gemm"]
 
-KERNEL_CLASSES = {"gje_update": 0, "gje_panel": 1, "zside_gemm": 2, "jacobi": 3, "qr": 4,
-                  "resid_gemm": 5, "newton_update": 6}
+KERNEL_CLASSES = {"gje_update": 0, "gje_panel": 1, "zside_gemm": 2, "eig": 3, "qr": 4,
+                  "resid_gemm": 5, "newton_update": 6, "dgemm": 7, "tc_gemm": 8, "qr_panel": 9,
+                  "tridiag": 10}
 
 
 def library_path() -> str:
@@ -109,6 +110,7 @@ def lib():
         L.lyap_tc_gemm.restype = C.c_int
         L.lyap_kernel_timing.argtypes = [C.c_int]
         L.lyap_kernel_stats.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+        L.lyap_kernel_work.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double)]
         for s in SYMBOLS:
             if s not in ("lyap_ir_default_options", "lyap_launch_count"):
                 getattr(L, s).restype = C.c_int
@@ -149,9 +151,12 @@ def kernel_timing(cls):
 
 
 def kernel_stats():
+    """(device ms, timed launches, algorithmic flops, algorithmic bytes) since kernel_timing()."""
     ms, n = C.c_double(0), C.c_int64(0)
+    fl, by = C.c_double(0), C.c_double(0)
     lib().lyap_kernel_stats(C.byref(ms), C.byref(n))
-    return ms.value, n.value
+    lib().lyap_kernel_work(C.byref(fl), C.byref(by))
+    return ms.value, n.value, fl.value, by.value
 
 
 def default_options(**kw) -> Options:

@@ -10,6 +10,7 @@
 #pragma once
 #include <type_traits>
 #include "common.cuh"
+#include "ktimer.h"
 
 namespace lyap {
 
@@ -235,6 +236,7 @@ int gemm_strided(cudaStream_t s, int M, int N, int K, Acc alpha,
     if (splits > 1) splits = ceil_div(K, kchunk);
     dim3 grid(ceil_div(N, BN), ceil_div(M, BM), splits);
     if constexpr (all_f64) {
+        KTimer kt(KC_DGEMM, s, 2.0 * M * N * K, 8.0 * ((double)M * K + (double)K * N + 2.0 * M * N));
         dgemm_dmma_kernel<<<grid, 128, 0, s>>>(M, N, K, kchunk, alpha, A, sam, sak, B, sbk, sbn, beta, C, scm,
                                                scn, splits > 1 ? work : nullptr);
     } else {

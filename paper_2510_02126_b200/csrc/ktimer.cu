@@ -47,6 +47,14 @@ void ktimer_begin(int cls, cudaStream_t s) {
     cudaEventRecord(*slot(g_used, 0), s);
 }
 
+double g_flops = 0.0, g_bytes = 0.0;
+void ktimer_work(int cls, double flops, double bytes) {
+    if (cls != g_enabled) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_flops += flops;
+    g_bytes += bytes;
+}
+
 void ktimer_end(int cls, cudaStream_t s) {
     if (cls != g_enabled) return;
     std::lock_guard<std::mutex> lk(g_mu);
@@ -63,6 +71,8 @@ extern "C" int lyap_kernel_timing(int cls) {
     g_enabled = cls;
     g_ms = 0.0;
     g_count = 0;
+    g_flops = 0.0;
+    g_bytes = 0.0;
     return LYAP_OK;
 }
 
@@ -72,5 +82,13 @@ extern "C" int lyap_kernel_stats(double *ms, int64_t *launches) {
     drain();
     if (ms) *ms = g_ms;
     if (launches) *launches = g_count;
+    return LYAP_OK;
+}
+
+extern "C" int lyap_kernel_work(double *flops, double *bytes) {
+    using namespace lyap;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (flops) *flops = g_flops;
+    if (bytes) *bytes = g_bytes;
     return LYAP_OK;
 }

@@ -47,12 +47,18 @@ qr_panel_kernel(int m, int j0, int jb, double *__restrict__ W, double *__restric
     } else {
         P = W + (long)j0 * m + j0;
     }
+    __shared__ double s_next;                    // sum_{i>jj} x_i^2 of the next column (look-ahead)
     __syncthreads();
+    {
+        double s0 = 0.0;
+        for (int i = 1 + tid; i < R; i += nt) s0 = fma(P[i], P[i], s0);
+        s0 = block_sum(s0, red);
+        if (tid == 0) s_next = s0;
+        __syncthreads();
+    }
     for (int jj = 0; jj < jb; jj++) {
         double *x = P + (long)jj * ldp;           // rows jj..R-1 are the active part
-        double s = 0.0;
-        for (int i = jj + 1 + tid; i < R; i += nt) s = fma(x[i], x[i], s);
-        s = block_sum(s, red);
+        const double s = s_next;
         if (tid == 0) {
             double x0 = x[jj];
             double nrm2 = s + x0 * x0;
@@ -69,16 +75,25 @@ qr_panel_kernel(int m, int j0, int jb, double *__restrict__ W, double *__restric
         const double tj = s_tau;
         if (tid == 0) { tau[j0 + jj] = tj; x[jj] = (tj == 0.0) ? x[jj] : s_v0; }   // x now holds v (rows jj..)
         __syncthreads();
-        // apply H_j to the remaining panel columns: one warp per column
-        if (tj != 0.0)
-            for (int cc = jj + 1 + wid; cc < jb; cc += nwb) {
-                double *y = P + (long)cc * ldp;
+        // apply H_j to the remaining panel columns: one warp per column; warp 0 owns
+        // column jj+1 and also returns its trailing norm for the next reflector
+        for (int cc = jj + 1 + wid; cc < jb; cc += nwb) {
+            double *y = P + (long)cc * ldp;
+            if (tj != 0.0) {
                 double d = 0.0;
                 for (int i = jj + lane; i < R; i += 32) d = fma(x[i], y[i], d);
                 d = warp_sum(d);
                 const double f = tj * d;
                 for (int i = jj + lane; i < R; i += 32) y[i] = fma(-f, x[i], y[i]);
             }
+            if (cc == jj + 1) {
+                __syncwarp();
+                double s2 = 0.0;
+                for (int i = jj + 2 + lane; i < R; i += 32) s2 = fma(y[i], y[i], s2);
+                s2 = warp_sum(s2);
+                if (lane == 0) s_next = s2;
+            }
+        }
         __syncthreads();
     }
     // write V (full columns of length m) and R-part of W; x[jj] (the v0) -> alpha
@@ -108,19 +123,24 @@ qr_panel_kernel(int m, int j0, int jb, double *__restrict__ W, double *__restric
         for (int c = 0; c < QB; c++) Tsh[tid][c] = 0.0;
     }
     __syncthreads();
-    if (tid < 32) {
+    if (tid < 32) {                 // row a of T in registers (see wy_T_kernel)
         const int a = tid;
-        for (int c = 0; c < jb; c++) {
-            const double tc = tau[j0 + c];
-            double sacc = 0.0;
-            if (a < c)
-                for (int l = a; l < c; l++) sacc = fma(Tsh[a][l], G[l][c], sacc);
-            __syncwarp();
-            if (a < c) Tsh[a][c] = -tc * sacc;
-            if (a == c) Tsh[a][c] = tc;
-            __syncwarp();
+        double Ta[QB];
+#pragma unroll
+        for (int c = 0; c < QB; c++) Ta[c] = 0.0;
+#pragma unroll
+        for (int c = 0; c < QB; c++) {
+            if (c < jb) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int l = 0; l < c; l++)
+                    if (l >= a) sacc = fma(Ta[l], G[l][c], sacc);
+                const double tc = tau[j0 + c];
+                Ta[c] = (a < c) ? -tc * sacc : ((a == c) ? tc : 0.0);
+            }
         }
-        for (int c = 0; c < QB; c++) Tp[a + c * QB] = Tsh[a][c];
+#pragma unroll
+        for (int c = 0; c < QB; c++) Tp[a + c * QB] = Ta[c];
     }
     for (long idx = tid; idx < (long)R * jb; idx += nt) {
         int i = (int)(idx % R), c = (int)(idx / R);
@@ -228,7 +248,10 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
         double *Tp = w.T + pi * QB * QB;
         const size_t smem = sizeof(double) * (size_t)(m - j0) * jb;
         const bool use_smem = smem <= 200 * 1024;
-        qr_panel_kernel<<<1, 512, use_smem ? smem : 0, s>>>(m, j0, jb, Wm, w.V, w.tau, Tp, use_smem ? 1 : 0);
+        {
+            KTimer kp(KC_QR_PANEL, s, 4.0 * (m - j0) * jb * jb, 16.0 * (m - j0) * jb);
+            qr_panel_kernel<<<1, 512, use_smem ? smem : 0, s>>>(m, j0, jb, Wm, w.V, w.tau, Tp, use_smem ? 1 : 0);
+        }
         LYAP_TRY(launched());
         qr_alpha_kernel<<<1, 32, 0, s>>>(m, j0, jb, w.V, w.tau, diag);
         LYAP_TRY(launched());

@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "lyap_internal.h"
+#include "ktimer.h"
 
 namespace cg = cooperative_groups;
 
@@ -652,21 +653,28 @@ __global__ void dc_sort_kernel(int p, const MergeInfo *__restrict__ mi, const do
 // One warp; column c is computed in parallel over its rows.
 __global__ void wy_T_kernel(int jb, const double *__restrict__ G, const double *__restrict__ tau, double *__restrict__ Tp)
 {
-    __shared__ double T[32][33];
+    // lane a keeps row a of T in registers (fully unrolled, static indexing); G is
+    // read as warp-wide broadcasts from shared memory
+    __shared__ double Gs[32][33];
     const int a = threadIdx.x;
-    for (int c = 0; c < 32; c++) T[a][c] = 0.0;
+    for (int c = 0; c < 32; c++) Gs[c][a] = (a < jb && c < jb) ? G[a + c * 32] : 0.0;   // Gs[l][c]... transposed load
     __syncwarp();
-    for (int c = 0; c < jb; c++) {
-        const double tc = tau[c];
-        double sacc = 0.0;
-        if (a < c)
-            for (int l = a; l < c; l++) sacc = fma(T[a][l], G[l + c * 32], sacc);
-        __syncwarp();
-        if (a < c) T[a][c] = -tc * sacc;
-        if (a == c) T[a][c] = tc;
-        __syncwarp();
+    double Ta[32];
+#pragma unroll
+    for (int c = 0; c < 32; c++) Ta[c] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 32; c++) {
+        if (c < jb) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int l = 0; l < c; l++)
+                if (l >= a) sacc = fma(Ta[l], Gs[c][l], sacc);
+            const double tc = tau[c];
+            Ta[c] = (a < c) ? -tc * sacc : ((a == c) ? tc : 0.0);
+        }
     }
-    for (int c = 0; c < 32; c++) Tp[a + c * 32] = T[a][c];
+#pragma unroll
+    for (int c = 0; c < 32; c++) Tp[a + c * 32] = Ta[c];
 }
 
 // eigenvalues descending + sign normalisation (largest |component| positive, lowest index)
@@ -763,6 +771,7 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
         TridArgs ta{p, W.A, W.R, d, e, tau, P};
         void *args[] = {&ta};
         const int need = ceil_div(p, 8);             // one warp per column
+        KTimer kt(KC_TRIDIAG, s, (4.0 / 3.0) * (double)p * p * p, 8.0 * (double)p * p);
         if (p >= 3 && p <= 1024 && need <= max_blocks) {
             static bool attr2 = false;
             if (!attr2) {

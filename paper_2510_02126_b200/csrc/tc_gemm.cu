@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include "common.cuh"
 #include "lyap_internal.h"
+#include "ktimer.h"
 
 namespace lyap {
 
@@ -213,6 +214,7 @@ int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const vo
         cudaFuncSetAttribute(tc_gemm_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM);
         attr = true;
     }
+    KTimer kt(KC_TCGEMM, s, 2.0 * M * N * K, 2.0 * ((double)M * K + (double)N * K + (beta != 0.f ? 2.0 : 1.0) * M * N));
     if (prec == LYAP_BF16)
         tc_gemm_kernel<__nv_bfloat16><<<grid, 128, tc::SMEM, s>>>(ma, mb, M, N, K, alpha, beta, (__nv_bfloat16 *)C,
                                                                    ldc, colmajor);
