@@ -202,7 +202,8 @@ int64_t lyap_launch_count(void);
 /* Kernel-class timing for the roofline report: after lyap_kernel_timing(cls)
  * every launch of class cls (0 Gauss-Jordan rank-b update GEMM, 1 pivoted
  * panel, 2 A_k^{-1} Z products, 3 Jacobi eigensolver, 4 Householder QR,
- * 5 fp64 A Z, 6 Newton update; -1 disables) is bracketed by CUDA events on its
+ * 5 fp64 A Z, 6 Newton update, 7 fp64 DMMA GEMM, 8 tcgen05 GEMM, 9 Householder
+ * panel, 10 tridiagonalisation, 11 compact-WY application; -1 disables) is bracketed by CUDA events on its
  * launch stream.  lyap_kernel_stats synchronises and returns the summed
  * device milliseconds and the number of timed launches since the last
  * lyap_kernel_timing call. */
@@ -210,7 +211,7 @@ int lyap_kernel_timing(int cls);
 int lyap_kernel_stats(double *ms, int64_t *launches);
 /* Algorithmic flops and bytes of the launches timed since lyap_kernel_timing
  * (classes 7 fp64 DMMA GEMM, 8 tcgen05 GEMM, 9 Householder panel, 10
- * tridiagonalisation report them). */
+ * tridiagonalisation, 11 compact-WY application report them). */
 int lyap_kernel_work(double *flops, double *bytes);
 
 #ifdef __cplusplus

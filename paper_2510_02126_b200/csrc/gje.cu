@@ -50,8 +50,8 @@ gje_panel_kernel(int n, int k, int b, T *__restrict__ A, T *__restrict__ X,
     int *sflag = pivl + 32;                                    // 1
     Acc *P = use_smem ? reinterpret_cast<Acc *>(sflag + 4) : Pglob;   // R*b (row-major, ld b)
 
-    for (long idx = tid; idx < (long)R * b; idx += nt) {
-        long r = idx / b; int c = (int)(idx % b);
+    for (int idx = tid; idx < R * b; idx += nt) {
+        const int r = idx / b, c = idx - r * b;
         P[idx] = to_acc<T>(A[(long)(k + r) * n + k + c]);
     }
     if (tid == 0) *sflag = 0;
@@ -141,8 +141,8 @@ gje_panel_kernel(int n, int k, int b, T *__restrict__ A, T *__restrict__ X,
     __syncthreads();
 
     // ---- X rows
-    for (long idx = tid; idx < (long)n * b; idx += nt) {
-        long i = idx / b; int c = (int)(idx % b);
+    for (int idx = tid; idx < n * b; idx += nt) {
+        const int i = idx / b, c = idx - i * b;
         Acc s = Acc(0);
         if (i >= k && i < k + b) {
             s = Tw[(i - k) * 32 + c];
@@ -150,7 +150,7 @@ gje_panel_kernel(int n, int k, int b, T *__restrict__ A, T *__restrict__ X,
             const Acc *row = P + (i - k) * b;
             for (int t = 0; t < b; t++) s = fma(-row[t], Lw[t * 32 + c], s);
         } else {
-            const T *arow = A + i * n + k;
+            const T *arow = A + (long)i * n + k;
             for (int t = 0; t < b; t++) s = fma(-to_acc<T>(arow[t]), Tw[t * 32 + c], s);
         }
         X[idx] = from_acc<T>(s);

@@ -15,7 +15,8 @@ enum KernelClass {
     KC_DGEMM = 7,        // fp64 DMMA GEMM kernel (all fp64 products)
     KC_TCGEMM = 8,       // tcgen05 16-bit GEMM kernel
     KC_QR_PANEL = 9,     // Householder panel kernel
-    KC_TRIDIAG = 10      // cooperative tridiagonalisation kernel
+    KC_TRIDIAG = 10,     // cooperative tridiagonalisation kernel
+    KC_WY = 11           // fused compact-WY block-reflector application
 };
 
 void ktimer_begin(int cls, cudaStream_t s);

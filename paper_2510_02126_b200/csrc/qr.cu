@@ -15,6 +15,7 @@
 #include <vector>
 #include "common.cuh"
 #include "gemm_simt.cuh"
+#include "wy.cuh"
 #include "lyap_internal.h"
 #include "ktimer.h"
 
@@ -22,107 +23,114 @@ namespace lyap {
 
 static constexpr int QB = 32;
 
+// Warp reduce-scatter: lane l ends with sum over the warp of d[l].  31 shuffles.
+__device__ __forceinline__ double reduce_scatter32(double (&d)[QB], int lane)
+{
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int k = 0; k < off; k++) {
+            const double send = upper ? d[k] : d[k + off];
+            const double keep = upper ? d[k + off] : d[k];
+            d[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    return d[0];
+}
+
 // Factor panel columns [j0, j0+jb) of W (m x n, ld m), rows j0..m-1.
 // Writes V (m x k, ld m; zero above the diagonal), tau, and T_panel (QB x QB).
+// Row-distributed: per reflector, every thread forms the dot products of v with all
+// panel columns for its rows (32 register accumulators), one warp reduce-scatter +
+// one shared-memory pass give the totals; the products with earlier columns are the
+// Gram entries V^T v needed for T, so T costs no extra pass.  Two block barriers per
+// column (the dots; the look-ahead norm of the next column).
+template <bool SM>
 __global__ void __launch_bounds__(512)
 qr_panel_kernel(int m, int j0, int jb, double *__restrict__ W, double *__restrict__ V,
-                double *__restrict__ tau, double *__restrict__ Tp, int use_smem)
+                double *__restrict__ tau, double *__restrict__ Tp)
 {
     extern __shared__ double smp[];
-    __shared__ double red[32];
-    __shared__ double s_alpha, s_tau, s_v0;
+    __shared__ double red[16][QB + 1];
+    __shared__ double rnorm[16];
     __shared__ double G[QB][QB + 1];
-    __shared__ double Tsh[QB][QB + 1];
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int lane = tid & 31, wid = tid >> 5, nwb = nt >> 5;
+    const int lane = tid & 31, wid = tid >> 5;
     const int R = m - j0;                          // panel rows j0..m-1
-    // panel P (R x jb, ld R): shared memory or the matrix itself
-    double *P = use_smem ? smp : nullptr;
-    const int ldp = use_smem ? R : m;
-    if (use_smem) {
-        for (long idx = tid; idx < (long)R * jb; idx += nt) {
-            int i = (int)(idx % R), c = (int)(idx / R);
-            P[idx] = W[(long)(j0 + c) * m + j0 + i];
-        }
-    } else {
-        P = W + (long)j0 * m + j0;
+    double *P = SM ? smp : W + (long)j0 * m + j0;
+    const int ldp = SM ? R : m;
+    if (SM) {
+        for (int c = 0; c < jb; c++)
+            for (int i = tid; i < R; i += nt) P[c * R + i] = W[(long)(j0 + c) * m + j0 + i];
     }
-    __shared__ double s_next;                    // sum_{i>jj} x_i^2 of the next column (look-ahead)
     __syncthreads();
     {
         double s0 = 0.0;
         for (int i = 1 + tid; i < R; i += nt) s0 = fma(P[i], P[i], s0);
-        s0 = block_sum(s0, red);
-        if (tid == 0) s_next = s0;
+        s0 = warp_sum(s0);
+        if (lane == 0) rnorm[wid] = s0;
         __syncthreads();
     }
     for (int jj = 0; jj < jb; jj++) {
-        double *x = P + (long)jj * ldp;           // rows jj..R-1 are the active part
-        const double s = s_next;
-        if (tid == 0) {
-            double x0 = x[jj];
-            double nrm2 = s + x0 * x0;
-            if (nrm2 == 0.0) { s_tau = 0.0; s_alpha = 0.0; s_v0 = 0.0; }
-            else {
-                double nrm = sqrt(nrm2);
-                double alpha = (x0 >= 0.0) ? -nrm : nrm;
-                double v0 = x0 - alpha;
-                s_alpha = alpha; s_v0 = v0;
-                s_tau = 2.0 / (v0 * v0 + s);
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < 16; w++) s += rnorm[w];
+        const double x0 = P[jj * ldp + jj];
+        double tj = 0.0, v0 = 0.0;
+        const double nrm2 = s + x0 * x0;
+        if (nrm2 != 0.0) {
+            const double alpha = (x0 >= 0.0) ? -sqrt(nrm2) : sqrt(nrm2);
+            v0 = x0 - alpha;
+            tj = 2.0 / (v0 * v0 + s);
+        }
+        // d[c] = v^T P[:, c] over rows jj..R-1 (c < jj: Gram entries v_c^T v)
+        double d[QB];
+#pragma unroll
+        for (int c = 0; c < QB; c++) d[c] = 0.0;
+        if (tj != 0.0) {
+            for (int i = jj + tid; i < R; i += nt) {
+                const double vi = (i == jj) ? v0 : P[jj * ldp + i];
+#pragma unroll
+                for (int c = 0; c < QB; c++)
+                    if (c < jb) d[c] = fma(vi, P[c * ldp + i], d[c]);
             }
         }
+        red[wid][lane] = reduce_scatter32(d, lane);
         __syncthreads();
-        const double tj = s_tau;
-        if (tid == 0) { tau[j0 + jj] = tj; x[jj] = (tj == 0.0) ? x[jj] : s_v0; }   // x now holds v (rows jj..)
-        __syncthreads();
-        // apply H_j to the remaining panel columns: one warp per column; warp 0 owns
-        // column jj+1 and also returns its trailing norm for the next reflector
-        for (int cc = jj + 1 + wid; cc < jb; cc += nwb) {
-            double *y = P + (long)cc * ldp;
-            if (tj != 0.0) {
-                double d = 0.0;
-                for (int i = jj + lane; i < R; i += 32) d = fma(x[i], y[i], d);
-                d = warp_sum(d);
-                const double f = tj * d;
-                for (int i = jj + lane; i < R; i += 32) y[i] = fma(-f, x[i], y[i]);
+        double dl = 0.0;
+#pragma unroll
+        for (int w = 0; w < 16; w++) dl += red[w][lane];
+        if (wid == 0 && lane < jj) G[lane][jj] = dl;
+#pragma unroll
+        for (int c = 0; c < QB; c++) d[c] = __shfl_sync(0xffffffffu, dl, c);
+        // apply H_jj to columns jj+1.. and the look-ahead norm of column jj+1
+        double s2 = 0.0;
+        for (int i = jj + tid; i < R; i += nt) {
+            const double vi = (i == jj) ? v0 : P[jj * ldp + i];
+            const double f = tj * vi;
+#pragma unroll
+            for (int c = 0; c < QB; c++) {
+                if (c > jj && c < jb) {
+                    const double y = fma(-f, d[c], P[c * ldp + i]);
+                    P[c * ldp + i] = y;
+                    if (c == jj + 1 && i > jj + 1) s2 = fma(y, y, s2);
+                }
             }
-            if (cc == jj + 1) {
-                __syncwarp();
-                double s2 = 0.0;
-                for (int i = jj + 2 + lane; i < R; i += 32) s2 = fma(y[i], y[i], s2);
-                s2 = warp_sum(s2);
-                if (lane == 0) s_next = s2;
-            }
+            if (i == jj && tj != 0.0) P[jj * ldp + jj] = v0;   // column jj now holds v
         }
+        if (tid == 0) tau[j0 + jj] = tj;
+        s2 = warp_sum(s2);
+        if (lane == 0) rnorm[wid] = s2;
         __syncthreads();
     }
-    // write V (full columns of length m) and R-part of W; x[jj] (the v0) -> alpha
-    for (long idx = tid; idx < (long)m * jb; idx += nt) {
-        int i = (int)(idx % m), c = (int)(idx / m);
+    // write V (full columns of length m); x[jj] holds v0
+    for (int c = 0; c < jb; c++) {
         const int j = j0 + c;
-        double vv = 0.0;
-        if (i >= j && tau[j] != 0.0) vv = P[(long)c * ldp + (i - j0)];
-        V[(long)j * m + i] = vv;
+        const bool nz = tau[j] != 0.0;
+        for (int i = tid; i < m; i += nt) V[(long)j * m + i] = (nz && i >= j) ? P[c * ldp + (i - j0)] : 0.0;
     }
-    __syncthreads();
-    // Gram of the panel's reflectors (warp per entry) -> T
-    for (int e = wid; e < jb * jb; e += nwb) {
-        int a = e / jb, c = e % jb;
-        double d = 0.0;
-        if (a <= c) {
-            const double *va = V + (long)(j0 + a) * m, *vc = V + (long)(j0 + c) * m;
-            for (int i = j0 + a + lane; i < m; i += 32) d = fma(va[i], vc[i], d);
-            d = warp_sum(d);
-        }
-        if (lane == 0) G[a][c] = d;
-    }
-    // R part: column j0+c of W: rows < j0 unchanged, rows j0..j0+c from P (above the
-    // diagonal) with the diagonal = alpha, below = 0
-    __syncthreads();
-    if (tid < 32) {
-        for (int c = 0; c < QB; c++) Tsh[tid][c] = 0.0;
-    }
-    __syncthreads();
+    __syncthreads();                // P may alias W (no shared-memory staging)
     if (tid < 32) {                 // row a of T in registers (see wy_T_kernel)
         const int a = tid;
         double Ta[QB];
@@ -142,17 +150,11 @@ qr_panel_kernel(int m, int j0, int jb, double *__restrict__ W, double *__restric
 #pragma unroll
         for (int c = 0; c < QB; c++) Tp[a + c * QB] = Ta[c];
     }
-    for (long idx = tid; idx < (long)R * jb; idx += nt) {
-        int i = (int)(idx % R), c = (int)(idx / R);
-        const int j = j0 + c;
-        double out;
-        if (i < c) out = P[(long)c * ldp + i];
-        else if (i == c) {
-            // diagonal: alpha (recomputed as -sign(x0)||x||: stored implicitly: R_jj = v0 - ... )
-            out = 0.0;   // filled below
-        } else out = 0.0;
-        if (i != c) W[(long)j * m + j0 + i] = out;
-    }
+    // R part of the panel columns: above the diagonal from P, below zero (the
+    // diagonal is written by qr_finish from alpha)
+    for (int c = 0; c < jb; c++)
+        for (int i = tid; i < R; i += nt)
+            if (i != c) W[(long)(j0 + c) * m + j0 + i] = (i < c) ? P[c * ldp + i] : 0.0;
 }
 
 // diagonal entries alpha_j = -sign(x0) ||x||: recovered from v0 and tau: with
@@ -230,7 +232,7 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
     double *diag = w.tau + k;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(qr_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
     LYAP_CUDA_TRY(cudaMemcpyAsync(Wm, A, sizeof(double) * (size_t)m * n, cudaMemcpyDeviceToDevice, s));
@@ -250,7 +252,8 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
         const bool use_smem = smem <= 200 * 1024;
         {
             KTimer kp(KC_QR_PANEL, s, 4.0 * (m - j0) * jb * jb, 16.0 * (m - j0) * jb);
-            qr_panel_kernel<<<1, 512, use_smem ? smem : 0, s>>>(m, j0, jb, Wm, w.V, w.tau, Tp, use_smem ? 1 : 0);
+            if (use_smem) qr_panel_kernel<true><<<1, 512, smem, s>>>(m, j0, jb, Wm, w.V, w.tau, Tp);
+            else qr_panel_kernel<false><<<1, 512, 0, s>>>(m, j0, jb, Wm, w.V, w.tau, Tp);
         }
         LYAP_TRY(launched());
         qr_alpha_kernel<<<1, 32, 0, s>>>(m, j0, jb, w.V, w.tau, diag);
@@ -259,14 +262,8 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
         if (nt > 0) {
             const double *Vp = w.V + (size_t)j0 * m;
             double *Wt = Wm + (size_t)(j0 + jb) * m;
-            // Y = V_p^T Wt (jb x nt)      (rows j0..m-1 suffice: V zero above)
-            LYAP_TRY(dgemm_cm(s, true, false, jb, nt, m - j0, 1.0, Vp + j0, m, Wt + j0, m, 0.0, w.W, QB));
-            // Y2 = T^T Y
-            LYAP_TRY(gemm_strided<double, double, double, double>(s, jb, nt, jb, 1.0, Tp, QB, 1, w.W, 1, QB,
-                                                                  0.0, w.W + (size_t)QB * nt, 1, QB));
-            // Wt -= V_p Y2
-            LYAP_TRY(dgemm_cm(s, false, false, m - j0, nt, jb, -1.0, Vp + j0, m, w.W + (size_t)QB * nt, QB, 1.0,
-                              Wt + j0, m));
+            // Wt <- (I - V T^T V^T) Wt, rows j0..m-1 (V is zero above)
+            LYAP_TRY(wy_apply(s, m, nt, jb, j0, Vp, m, Tp, 1, Wt, m));
         }
     }
     // Q = H_0 ... H_{k-1} [I; 0]
@@ -278,11 +275,7 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
         const double *Vp = w.V + (size_t)j0 * m;
         int nc = k - j0;               // columns j0..k-1 of Q are affected
         double *Qc = Q + (size_t)j0 * m;
-        LYAP_TRY(dgemm_cm(s, true, false, jb, nc, m - j0, 1.0, Vp + j0, m, Qc + j0, m, 0.0, w.W, QB));
-        LYAP_TRY(gemm_strided<double, double, double, double>(s, jb, nc, jb, 1.0, Tp, 1, QB, w.W, 1, QB,
-                                                              0.0, w.W + (size_t)QB * nc, 1, QB));
-        LYAP_TRY(dgemm_cm(s, false, false, m - j0, nc, jb, -1.0, Vp + j0, m, w.W + (size_t)QB * nc, QB, 1.0,
-                          Qc + j0, m));
+        LYAP_TRY(wy_apply(s, m, nc, jb, j0, Vp, m, Tp, 0, Qc, m));
     }
     int tot = (int)(((long)k * n + (long)m * k + 255) / 256);
     qr_finish_kernel<<<tot < 1024 ? tot : 1024, 256, 0, s>>>(m, n, k, Wm, diag, Q, R);

@@ -21,6 +21,7 @@
 #include <cmath>
 #include "common.cuh"
 #include "gemm_simt.cuh"
+#include "wy.cuh"
 #include "lyap_internal.h"
 #include "ktimer.h"
 
@@ -857,11 +858,8 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
         LYAP_TRY(dgemm_cm(s, true, false, jb, jb, p, 1.0, Vp, p, Vp, p, 0.0, W.Qk, 32));
         wy_T_kernel<<<1, 32, 0, s>>>(jb, W.Qk, tau + j0, Tp);
         LYAP_TRY(launched());
-        // Wt = V^T X (jb x p) ; Wt2 = T Wt ; X -= V Wt2
-        LYAP_TRY(dgemm_cm(s, true, false, jb, p, p, 1.0, Vp, p, W.Q, p, 0.0, W.Qk, 32));
-        LYAP_TRY(gemm_strided<double, double, double, double>(s, jb, p, jb, 1.0, Tp, 1, 32, W.Qk, 1, 32, 0.0,
-                                                              W.U, 1, 32));
-        LYAP_TRY(dgemm_cm(s, false, false, p, p, jb, -1.0, Vp, p, W.U, 32, 1.0, W.Q, p));
+        // X <- (I - V T V^T) X over rows j0+1..p-1 (reflector j0+a is zero above row j0+a+1)
+        LYAP_TRY(wy_apply(s, p, p, jb, j0 + 1, Vp, p, Tp, 0, W.Q, p));
     }
     eigfinal_kernel<<<std::min(ceil_div((long)p * 32, 256), 1024), 256, 0, s>>>(p, lam, W.Q, w_out, V_out);
     LYAP_TRY(launched());

@@ -306,7 +306,7 @@ def test_ir_cfg1_full_size(gpu, orc):
     """configs[1] at full size (n=1024, LDL^T, bf16): the oracle's IR (emulated bf16)
     and the GPU path agree."""
     p = P.cfg1()
-    res, ro, Xg, Xo, W = _ir_parity(gpu, orc, p, "bf16", ldlt=True, maxit=30, max_cols=256)
+    res, ro, Xg, Xo, W = _ir_parity(gpu, orc, p, "bf16", ldlt=True, maxit=30, max_cols=640)
     assert res.report["status"] == ro.status
     assert res.report["steps"] == ro.steps
     assert orc.rel_residual_explicit(p.A, Xg, W) <= 1e-13

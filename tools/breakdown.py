@@ -16,6 +16,6 @@ s = G.Solver(p.n, us=wl["us"], max_cols=mc)
 t = time.time(); r = s.solve(A, Lt, S, tol=wl["tol"], maxit=wl["maxit"]); torch.cuda.synchronize()
 print("solve wall %.3f s" % (time.time() - t), {k: v for k, v in r.report.items() if k not in ("res",)})
 for name in G.KERNEL_CLASSES:
-    G.kernel_timing(name); s.solve(A, Lt, S, tol=wl["tol"], maxit=wl["maxit"]); ms, c = G.kernel_stats()
+    G.kernel_timing(name); s.solve(A, Lt, S, tol=wl["tol"], maxit=wl["maxit"]); ms, c = G.kernel_stats()[:2]
     print(f"{name:14s} {ms:10.2f} ms  {c:6d} launches")
 G.kernel_timing(None)
