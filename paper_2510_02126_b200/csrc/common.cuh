@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <algorithm>
 #include "../../include/lyap_ir.h"
@@ -42,6 +43,12 @@ inline int launched() {
 }
 
 inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
+
+// debugging switches read once per process (LYAP_QR_1CTA=1 etc.)
+inline bool env_flag(const char *name) {
+    const char *e = getenv(name);
+    return e && e[0] && e[0] != '0';
+}
 
 // ---------------------------------------------------------------- precision
 template <typename T> struct Prec;

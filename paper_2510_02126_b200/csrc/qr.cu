@@ -13,6 +13,7 @@
 // The sign convention diag(R) >= 0 makes the factorization unique for full
 // column rank, so it matches any other Householder QR up to rounding.
 #include <vector>
+#include <cooperative_groups.h>
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "wy.cuh"
@@ -157,9 +158,185 @@ qr_panel_kernel(int m, int j0, int jb, double *__restrict__ W, double *__restric
             if (i != c) W[(long)(j0 + c) * m + j0 + i] = (i < c) ? P[c * ldp + i] : 0.0;
 }
 
-// diagonal entries alpha_j = -sign(x0) ||x||: recovered from v0 and tau: with
-// v0 = x0 - alpha and tau = 2/(v^T v) = 1/(||x|| (||x|| + |x0|)) -> alpha = x0 - v0.
-// The panel kernel keeps x0 implicitly; we store alpha separately instead.
+// ---------------------------------------------------------------------------------
+// Cluster panel: the same reflectors as qr_panel_kernel, with the panel's rows split
+// over a cluster of QC CTAs (one SM each).  Every CTA keeps its RB-row slice of the
+// 32-column panel in shared memory; per reflector the partial dot products (E1) and
+// the look-ahead norm plus the next pivot entry (E2) are exchanged through
+// distributed shared memory with one cluster barrier each.
+constexpr int QC = 8, QCT = 256;
+
+__device__ __forceinline__ double reduce_scatter16(double (&d)[16], int lane)
+{
+#pragma unroll
+    for (int off = 8; off >= 1; off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int k = 0; k < off; k++) {
+            const double send = upper ? d[k] : d[k + off];
+            const double keep = upper ? d[k + off] : d[k];
+            d[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    return d[0] + __shfl_xor_sync(0xffffffffu, d[0], 16);   // lane l: column (l & 15)
+}
+
+__global__ void __cluster_dims__(QC, 1, 1) __launch_bounds__(QCT)
+qr_panel_cluster_kernel(int m, int j0, int jb, int RB, double *__restrict__ W, double *__restrict__ V,
+                        double *__restrict__ tau, double *__restrict__ diag, double *__restrict__ Tp)
+{
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double Pl[];                 // RB x QB, column-major (ld RB)
+    __shared__ double xch0[QB];                    // E1: this CTA's partial dots
+    __shared__ double xch1[16];                    // E2: per warp (norm partial, next pivot entry)
+    __shared__ double part[8][16];
+    __shared__ double G[QB][QB + 1];
+    __shared__ double tl[QB];                      // tau of this panel (every CTA has it)
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int q = (int)cl.block_rank();
+    const int R = m - j0;
+    const int g0 = q * RB;                         // first panel row of this CTA
+    const int nloc = max(0, min(RB, R - g0));
+    const int h = tid >> 7, lr0 = tid & 127;       // column half, first local row
+    for (int c = 0; c < jb; c++)
+        for (int i = tid; i < nloc; i += QCT) Pl[c * RB + i] = W[(long)(j0 + c) * m + j0 + g0 + i];
+    __syncthreads();
+    // E2 for column 0: norm of rows 1.. and the pivot entry
+    {
+        double s0 = 0.0, x0p = 0.0;
+        if (h == 0)
+            for (int i = lr0; i < nloc; i += 128) {
+                const double x = Pl[i];
+                if (g0 + i >= 1) s0 = fma(x, x, s0);
+                else x0p = x;
+            }
+        s0 = warp_sum(s0);
+        x0p = warp_sum(x0p);
+        if (lane == 0) { xch1[2 * wid] = s0; xch1[2 * wid + 1] = x0p; }
+    }
+    auto gather_e2 = [&](double &s, double &x0) {
+        const double *rem = cl.map_shared_rank(xch1, lane >> 2);
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int t = 0; t < 2; t++) {
+            a += rem[(lane & 3) * 4 + 2 * t];
+            b += rem[(lane & 3) * 4 + 2 * t + 1];
+        }
+        s = warp_sum(a);
+        x0 = warp_sum(b);
+    };
+    cl.sync();
+    double s, x0;
+    gather_e2(s, x0);
+    for (int jj = 0; jj < jb; jj++) {
+        double tj = 0.0, v0 = 0.0, alpha = 0.0;
+        const double nrm2 = s + x0 * x0;
+        if (nrm2 != 0.0) {
+            alpha = (x0 >= 0.0) ? -sqrt(nrm2) : sqrt(nrm2);
+            v0 = x0 - alpha;
+            tj = 2.0 / (v0 * v0 + s);
+        }
+        // E1: d[c] = v^T P[:, c] (c < jj: Gram entries v_c^T v)
+        double d[16];
+#pragma unroll
+        for (int c = 0; c < 16; c++) d[c] = 0.0;
+        if (tj != 0.0) {
+            for (int i = lr0; i < nloc; i += 128) {
+                const int gi = g0 + i;
+                if (gi < jj) continue;
+                const double vi = (gi == jj) ? v0 : Pl[jj * RB + i];
+#pragma unroll
+                for (int c = 0; c < 16; c++)
+                    if (h * 16 + c < jb) d[c] = fma(vi, Pl[(h * 16 + c) * RB + i], d[c]);
+            }
+        }
+        const double wv = reduce_scatter16(d, lane);
+        if (lane < 16) part[wid][lane] = wv;
+        __syncthreads();
+        if (tid < QB) {
+            const int hb = (tid >> 4) * 4;
+            xch0[tid] = part[hb][tid & 15] + part[hb + 1][tid & 15] + part[hb + 2][tid & 15] + part[hb + 3][tid & 15];
+        }
+        cl.sync();
+        double dt = 0.0;
+        {
+            const int col = h * 16 + (lane & 15);
+#pragma unroll
+            for (int r = 0; r < QC / 2; r++) dt += cl.map_shared_rank(xch0, 2 * r + (lane >> 4))[col];
+            dt += __shfl_xor_sync(0xffffffffu, dt, 16);
+            if (q == 0 && lane < 16 && col < jj) G[col][jj] = dt;
+        }
+#pragma unroll
+        for (int c = 0; c < 16; c++) d[c] = __shfl_sync(0xffffffffu, dt, c);
+        // apply H_jj to columns jj+1.., look-ahead norm and pivot entry of column jj+1
+        double s2 = 0.0, xn = 0.0;
+        for (int i = lr0; i < nloc; i += 128) {
+            const int gi = g0 + i;
+            if (gi < jj) continue;
+            const double vi = (gi == jj) ? v0 : Pl[jj * RB + i];
+            const double f = tj * vi;
+#pragma unroll
+            for (int c = 0; c < 16; c++) {
+                const int cc = h * 16 + c;
+                if (cc > jj && cc < jb) {
+                    const double y = fma(-f, d[c], Pl[cc * RB + i]);
+                    Pl[cc * RB + i] = y;
+                    if (cc == jj + 1) {
+                        if (gi > jj + 1) s2 = fma(y, y, s2);
+                        else if (gi == jj + 1) xn = y;
+                    }
+                }
+            }
+            if (gi == jj && h == 0 && tj != 0.0) Pl[jj * RB + i] = v0;   // column jj now holds v
+        }
+        if (tid == 0) {
+            tl[jj] = tj;
+            if (q == 0) { tau[j0 + jj] = tj; diag[j0 + jj] = (tj == 0.0) ? 0.0 : alpha; }
+        }
+        s2 = warp_sum(s2);
+        xn = warp_sum(xn);
+        if (lane == 0) { xch1[2 * wid] = s2; xch1[2 * wid + 1] = xn; }
+        cl.sync();
+        gather_e2(s, x0);
+    }
+    // V (full columns of length m), the R part above the diagonal, T from the Gram entries
+    for (int c = 0; c < jb; c++) {
+        const int j = j0 + c;
+        const bool nz = tl[c] != 0.0;
+        for (int i = tid; i < nloc; i += QCT) {
+            const int gi = g0 + i;
+            const double pv = Pl[c * RB + i];
+            V[(long)j * m + j0 + gi] = (nz && gi >= c) ? pv : 0.0;
+            if (gi != c) W[(long)j * m + j0 + gi] = (gi < c) ? pv : 0.0;
+        }
+        if (q == 0)
+            for (int i = tid; i < j0; i += QCT) V[(long)j * m + i] = 0.0;
+    }
+    if (q == 0) {
+        __syncthreads();
+        if (tid < 32) {
+            const int a = tid;
+            double Ta[QB];
+#pragma unroll
+            for (int c = 0; c < QB; c++) Ta[c] = 0.0;
+#pragma unroll
+            for (int c = 0; c < QB; c++) {
+                if (c < jb) {
+                    double sacc = 0.0;
+#pragma unroll
+                    for (int l = 0; l < c; l++)
+                        if (l >= a) sacc = fma(Ta[l], G[l][c], sacc);
+                    const double tc = tl[c];
+                    Ta[c] = (a < c) ? -tc * sacc : ((a == c) ? tc : 0.0);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < QB; c++) Tp[a + c * QB] = Ta[c];
+        }
+    }
+    cl.sync();                                     // no CTA leaves while its shared memory may be read
+}
 
 __global__ void set_identity_kernel(int m, int k, double *Q) {
     long tot = (long)m * k;
@@ -233,14 +410,17 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(qr_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(qr_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
     LYAP_CUDA_TRY(cudaMemcpyAsync(Wm, A, sizeof(double) * (size_t)m * n, cudaMemcpyDeviceToDevice, s));
-    // panel widths: 32, or 16/8 while the panel would not fit in shared memory
+    // cluster panels (32 wide) while a CTA's row slice fits in shared memory; otherwise
+    // the one-CTA panel with widths 32, or 16/8 while the panel would not fit
+    const bool use_cluster = ceil_div(m, QC) * QB * sizeof(double) <= 200 * 1024 && !env_flag("LYAP_QR_1CTA");
     std::vector<int> starts;
     for (int j0 = 0, jb; j0 < k; j0 += jb) {
         jb = QB;
-        while (jb > 8 && sizeof(double) * (size_t)(m - j0) * jb > 200 * 1024) jb /= 2;
+        while (!use_cluster && jb > 8 && sizeof(double) * (size_t)(m - j0) * jb > 200 * 1024) jb /= 2;
         jb = std::min(jb, k - j0);
         starts.push_back(j0);
     }
@@ -248,16 +428,24 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
     for (size_t pi = 0; pi + 1 < starts.size(); pi++) {
         const int j0 = starts[pi], jb = starts[pi + 1] - j0;
         double *Tp = w.T + pi * QB * QB;
-        const size_t smem = sizeof(double) * (size_t)(m - j0) * jb;
-        const bool use_smem = smem <= 200 * 1024;
-        {
+        if (use_cluster) {
+            const int RB = ceil_div(m - j0, QC);
             KTimer kp(KC_QR_PANEL, s, 4.0 * (m - j0) * jb * jb, 16.0 * (m - j0) * jb);
-            if (use_smem) qr_panel_kernel<true><<<1, 512, smem, s>>>(m, j0, jb, Wm, w.V, w.tau, Tp);
-            else qr_panel_kernel<false><<<1, 512, 0, s>>>(m, j0, jb, Wm, w.V, w.tau, Tp);
+            qr_panel_cluster_kernel<<<QC, QCT, sizeof(double) * RB * QB, s>>>(m, j0, jb, RB, Wm, w.V, w.tau, diag,
+                                                                           Tp);
+            LYAP_TRY(launched());
+        } else {
+            const size_t smem = sizeof(double) * (size_t)(m - j0) * jb;
+            const bool use_smem = smem <= 200 * 1024;
+            {
+                KTimer kp(KC_QR_PANEL, s, 4.0 * (m - j0) * jb * jb, 16.0 * (m - j0) * jb);
+                if (use_smem) qr_panel_kernel<true><<<1, 512, smem, s>>>(m, j0, jb, Wm, w.V, w.tau, Tp);
+                else qr_panel_kernel<false><<<1, 512, 0, s>>>(m, j0, jb, Wm, w.V, w.tau, Tp);
+            }
+            LYAP_TRY(launched());
+            qr_alpha_kernel<<<1, 32, 0, s>>>(m, j0, jb, w.V, w.tau, diag);
+            LYAP_TRY(launched());
         }
-        LYAP_TRY(launched());
-        qr_alpha_kernel<<<1, 32, 0, s>>>(m, j0, jb, w.V, w.tau, diag);
-        LYAP_TRY(launched());
         int nt = n - (j0 + jb);
         if (nt > 0) {
             const double *Vp = w.V + (size_t)j0 * m;
