@@ -340,12 +340,54 @@ def run_gpu(args):
         "clocks": clk.summary(),
         "residuals_all_ranks": [r.item() for r in all_res],
     }
+    if args.scale != "none":
+        line["sign_newton_at_scale"] = sign_newton_scale(G, P, dev, pk, args.scale)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(wl, p)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def sign_newton_scale(G, P, dev, pk, which):
+    """The sign-Newton A-sequence (the u_s inversions, Eq. newton-lyapu1) at a larger
+    configuration's size: TFLOP/s of the whole sequence and of its tensor-core GEMM."""
+    import torch
+    p = getattr(P, which)()
+    n = p.n
+    A = torch.tensor(p.A, dtype=torch.float64, device=dev)
+    del p
+    s = G.Solver(n, us="fp16", max_cols=64)
+    out = s.newton_aseq(A)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 2
+    e0.record()
+    for _ in range(reps):
+        out = s.newton_aseq(A)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    k = out["steps"]
+    flops = k * 2.0 * n ** 3                      # Gauss-Jordan inversion: 2 n^3 per Newton step
+    res = {"workload": f"{which}: n={n} fp16 sign-Newton A-sequence ({k} inversions)", "ms": ms,
+           "tflops": flops / (ms / 1e3) / 1e12}
+    res["frac_of_fp16_peak"] = res["tflops"] / pk["bf16"]
+    classes = {}
+    for name in ("tc_gemm", "gje_panel", "gje_update"):
+        G.kernel_timing(name)
+        s.newton_aseq(A)
+        classes[name] = G.kernel_stats()
+    G.kernel_timing(None)
+    ms_t, cnt, fl, _ = classes["tc_gemm"]
+    ach = fl / (ms_t / 1e3) / 1e12 if ms_t > 0 else 0.0
+    res["tc_gemm"] = {"bound": "tensor", "achieved": ach, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
+                      "frac": ach / pk["bf16_sus"], "launches": cnt, "ms": ms_t}
+    res["class_ms"] = {k2: v[0] for k2, v in classes.items()}
+    del s, A
+    torch.cuda.empty_cache()
+    return res
 
 
 def importlib_build():
@@ -362,6 +404,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg1", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scale", default="cfg2", choices=["none", "cfg2", "cfg3"],
+                    help="also time the fp16 sign-Newton A-sequence at this configuration's n (rank 0)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3

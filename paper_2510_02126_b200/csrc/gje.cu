@@ -16,6 +16,7 @@
 // = A[:, i]; the caller gathers columns with invperm.  The pivot sequence is
 // exactly that of LU with partial pivoting (the rows below the block see the
 // same Schur complement as right-looking LU).
+#include <cooperative_groups.h>
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "lyap_internal.h"
@@ -177,6 +178,234 @@ gje_panel_kernel(int n, int k, int b, T *__restrict__ A, T *__restrict__ X,
     }
 }
 
+// -------------------------------------------------------------- cluster panel
+// The same panel factorisation with the R = n-k panel rows split over a thread-block
+// cluster of NC CTAs (one SM each, RB >= b rows per CTA).  Each thread keeps RPT panel
+// rows in registers.  Per column one cluster exchange: every CTA publishes its local
+// pivot candidate (|value|, row, the row itself) and, if it owns it, the current row
+// j; after the cluster barrier every warp picks the same winner (largest |value|,
+// lowest row on ties -- the single-CTA rule), the pivot row is broadcast by warp
+// shuffles, and each thread swaps/eliminates its own rows.  Every matrix element
+// sees exactly the arithmetic of the single-CTA kernel, so pivots and results are
+// bitwise identical.
+template <typename Acc, int BW>
+__device__ __forceinline__ Acc sel_col(const Acc (&r)[BW], int j) {
+    Acc v = r[0];
+#pragma unroll
+    for (int c = 1; c < BW; c++) v = (c == j) ? r[c] : v;
+    return v;
+}
+
+template <typename T, int BW, int RPT>
+__global__ void __launch_bounds__(512)
+gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T *__restrict__ X,
+                         int *__restrict__ ipiv, int *__restrict__ moved, int *__restrict__ nmoved,
+                         int *__restrict__ info, typename Prec<T>::acc *__restrict__ Tglob)
+{
+    namespace cg = cooperative_groups;
+    using Acc = typename Prec<T>::acc;
+    constexpr int NT = 512;
+    cg::cluster_group cl = cg::this_cluster();
+    const int q = (int)cl.block_rank(), NC = (int)cl.num_blocks();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int R = n - k;
+    const int g0 = q * RB, nloc = max(0, min(RB, R - g0));
+    constexpr int PW = 2 + 2 * BW;                             // |cand|, row index, cand row, row j
+    __shared__ Acc pub[2][PW];
+    __shared__ Acc inbox[2][16][PW];                           // pushed by every CTA of the cluster
+    __shared__ Acc redv[16];
+    __shared__ int redi[16];
+    __shared__ int pivl[32];
+    __shared__ int sflag;
+    __shared__ Acc Ptop[32][33];
+    __shared__ Acc Lw[32 * 32], Tw[32 * 32];
+    Acc row[RPT][BW];
+#pragma unroll
+    for (int h = 0; h < RPT; h++) {
+        const int r = tid + NT * h;
+        const T *src = A + (long)(k + g0 + r) * n + k;
+#pragma unroll
+        for (int c = 0; c < BW; c++) row[h][c] = (r < nloc && c < b) ? to_acc<T>(src[c]) : Acc(0);
+    }
+    if (tid == 0) sflag = 0;
+    // columns unrolled: every register index and every (c > j) test is a compile-time constant
+#pragma unroll
+    for (int j = 0; j < BW; j++) {
+        if (j >= b) break;
+        const int buf = j & 1;
+        // ---- local candidate: max |P[r][j]|, panel row >= j, lowest row on ties
+        Acc bv = Acc(-1); int bi = R;
+#pragma unroll
+        for (int h = 0; h < RPT; h++) {
+            const int r = tid + NT * h, gi = g0 + r;
+            if (r < nloc && gi >= j) argmax_merge(bv, bi, fabs(row[h][j]), gi);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            Acc v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+            int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+            argmax_merge(bv, bi, v2, i2);
+        }
+        if (lane == 0) { redv[wid] = bv; redi[wid] = bi; }
+        __syncthreads();
+        bv = lane < 16 ? redv[lane] : Acc(-1);
+        bi = lane < 16 ? redi[lane] : R;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {                     // every lane needs the CTA winner
+            Acc v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+            int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+            argmax_merge(bv, bi, v2, i2);
+        }
+        if (tid == 0) { pub[buf][0] = bv; pub[buf][1] = Acc(bi); }
+#pragma unroll
+        for (int h = 0; h < RPT; h++) {
+            const int r = tid + NT * h, gi = g0 + r;
+            if (r < nloc && gi == bi)
+#pragma unroll
+                for (int c = 0; c < BW; c++) pub[buf][2 + c] = row[h][c];
+            if (r < nloc && gi == j)
+#pragma unroll
+                for (int c = 0; c < BW; c++) pub[buf][2 + BW + c] = row[h][c];
+        }
+        __syncthreads();
+        // ---- push this CTA's candidate (and row j) into every CTA's inbox
+        if (wid < NC) {
+            Acc *dst = cl.map_shared_rank(&inbox[buf][q][0], wid);
+            for (int e = lane; e < PW; e += 32) dst[e] = pub[buf][e];
+        }
+        cl.sync();
+        // ---- global winner from the local inbox, pivot row read as shared-memory broadcasts
+        Acc gbv = Acc(-1); int gbi = R;
+        for (int w = 0; w < NC; w++) argmax_merge(gbv, gbi, inbox[buf][w][0], (int)inbox[buf][w][1]);
+        const int pr = gbi < R ? gbi : j;                      // empty column: no swap (info is set)
+        const Acc *pvp = &inbox[buf][pr / RB][2];
+        const Acc *rjp = &inbox[buf][j / RB][2 + BW];
+        if (tid == 0) {
+            pivl[j] = pr;
+            if (!(gbv > Acc(0)) && sflag == 0) sflag = k + j + 1;
+        }
+        const Acc d = pvp[j];
+        const Acc inv = (d != Acc(0)) ? Acc(1) / d : Acc(0);
+#pragma unroll
+        for (int h = 0; h < RPT; h++) {
+            const int r = tid + NT * h, gi = g0 + r;
+            if (r >= nloc) continue;
+            if (gi == j) {
+                if (pr != j)
+#pragma unroll
+                    for (int c = 0; c < BW; c++) row[h][c] = pvp[c];
+            } else if (gi > j) {
+                if (gi == pr)
+#pragma unroll
+                    for (int c = 0; c < BW; c++) row[h][c] = rjp[c];
+                if (d != Acc(0)) {
+                    const Acc l = row[h][j] * inv;
+                    row[h][j] = l;
+#pragma unroll
+                    for (int c = j + 1; c < BW; c++) row[h][c] = fma(-l, pvp[c], row[h][c]);
+                }
+            }
+        }
+    }
+    // ---- Linv = L11^{-1}, Uinv = U11^{-1}, T = Uinv Linv on CTA 0 (owns panel rows 0..b-1);
+    // same recurrences and summation order as the single-CTA kernel, loops unrolled
+    if (q == 0 && tid < b) {
+#pragma unroll
+        for (int c = 0; c < BW; c++) if (c < b) Ptop[tid][c] = row[0][c];
+    }
+    __syncthreads();
+    if (q == 0) {
+        Acc *Uw = Tw;
+        if (tid < b) {
+            const int c = tid;
+            for (int i = 0; i < b; i++) {
+                Acc sacc = (i == c) ? Acc(1) : Acc(0);
+#pragma unroll
+                for (int t = 0; t < BW; t++)
+                    if (t >= c && t < i) sacc = fma(-Ptop[i][t], Lw[t * 32 + c], sacc);
+                Lw[i * 32 + c] = (i < c) ? Acc(0) : sacc;
+            }
+        } else if (tid >= 32 && tid < 32 + b) {
+            const int c = tid - 32;
+            for (int i = b - 1; i >= 0; i--) {
+                Acc sacc = (i == c) ? Acc(1) : Acc(0);
+#pragma unroll
+                for (int t = 1; t < BW; t++)
+                    if (t >= i + 1 && t <= c) sacc = fma(-Ptop[i][t], Uw[t * 32 + c], sacc);
+                Uw[i * 32 + c] = (i > c) ? Acc(0) : sacc / Ptop[i][i];
+            }
+        } else if (tid >= 64 && tid < 96) {
+            // moved rows: replay the transpositions on the candidate positions (one warp)
+            __shared__ int cand[64], src[64];
+            __shared__ int ncand;
+            const int ln = tid - 64;
+            cand[ln] = ln; src[ln] = ln;
+            if (ln == 0) ncand = b;
+            __syncwarp();
+            for (int j = 0; j < b; j++) {
+                const int pj = pivl[j];
+                const int nc0 = ncand;
+                const unsigned hit0 = __ballot_sync(0xffffffffu, ln < nc0 && cand[ln] == pj);
+                const unsigned hit1 = __ballot_sync(0xffffffffu, ln + 32 < nc0 && cand[ln + 32] == pj);
+                int ip = hit0 ? __ffs(hit0) - 1 : (hit1 ? 32 + __ffs(hit1) - 1 : -1);
+                if (ip < 0) {
+                    ip = nc0;
+                    if (ln == 0) { cand[ip] = pj; src[ip] = pj; ncand = nc0 + 1; }
+                }
+                __syncwarp();
+                if (ln == 0) { const int t = src[j]; src[j] = src[ip]; src[ip] = t; }
+                __syncwarp();
+            }
+            if (ln == 0) {
+                int mm = 0;
+                for (int t = 0; t < ncand; t++)
+                    if (src[t] != cand[t]) { moved[2 * mm] = cand[t]; moved[2 * mm + 1] = src[t]; mm++; }
+                *nmoved = mm;
+                for (int j = 0; j < b; j++) ipiv[k + j] = k + pivl[j];
+                if (sflag && *info == 0) *info = sflag;
+            }
+        }
+        __syncthreads();
+        Acc tval[2] = {Acc(0), Acc(0)};                        // 512 threads: rows ti and ti + 16
+        const int ti = tid / 32, tc = tid % 32;
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++)
+            if (ti + 16 * hh < b && tc < b)
+#pragma unroll
+                for (int t = 0; t < BW; t++)
+                    if (t < b) tval[hh] = fma(Uw[(ti + 16 * hh) * 32 + t], Lw[t * 32 + tc], tval[hh]);
+        __syncthreads();
+        for (int hh = 0; hh < 2; hh++)
+            if (ti + 16 * hh < b && tc < b) Tw[(ti + 16 * hh) * 32 + tc] = tval[hh];
+    }
+    cl.sync();
+    if (q != 0) {
+        const Acc *rL = cl.map_shared_rank(Lw, 0), *rT = cl.map_shared_rank(Tw, 0);
+        for (int e = tid; e < 32 * 32; e += NT) { Lw[e] = rL[e]; Tw[e] = rT[e]; }
+    }
+    __syncthreads();
+    // ---- X rows: own panel rows (block rows from T, rows below -L21 L11^{-1}), rows
+    // above the panel split evenly over the cluster
+#pragma unroll
+    for (int h = 0; h < RPT; h++) {
+        const int r = tid + NT * h, gi = g0 + r;
+        if (r >= nloc) continue;
+        T *xr = X + (long)(k + gi) * b;
+        for (int c = 0; c < b; c++) {
+            Acc sacc = Acc(0);
+            if (gi < b) sacc = Tw[gi * 32 + c];
+            else
+#pragma unroll
+                for (int t = 0; t < BW; t++) if (t < b) sacc = fma(-row[h][t], Lw[t * 32 + c], sacc);
+            xr[c] = from_acc<T>(sacc);
+        }
+    }
+    // rows above the panel: gje_xabove_kernel (the whole GPU), from T in global memory
+    if (q == 0)
+        for (int e = tid; e < 32 * 32; e += NT) Tglob[e] = Tw[e];
+    cl.sync();                                                 // shared memory stays valid for remote readers
+}
+
 // gather moved source rows (full width) and their rowperm entries into tmp
 template <typename T>
 __global__ void gje_gather_kernel(int n, int k, const T *__restrict__ A, const int *__restrict__ moved,
@@ -193,35 +422,161 @@ __global__ void gje_gather_kernel(int n, int k, const T *__restrict__ A, const i
 }
 
 // scatter moved rows, build B = pivot rows with B[:, panel] = I, zero pivot rows
-// and the panel columns of A.
+// and the panel columns of A, for the columns [c0, c1) (all n, or the outer block of
+// the two-level scheme).  O(b n) work: blockIdx.y < b are the block rows, the next
+// 2b the moved-row slots, the rest zero the panel columns of all other rows.
 template <typename T>
-__global__ void gje_prep_kernel(int n, int k, int b, T *__restrict__ A, const int *__restrict__ moved,
-                                const int *__restrict__ nmoved, const T *__restrict__ tmp,
-                                const int *__restrict__ tmp_perm, int *__restrict__ rowperm,
-                                T *__restrict__ B)
+__global__ void gje_prep_kernel(int n, int k, int b, int c0, int c1, T *__restrict__ A,
+                                const int *__restrict__ moved, const int *__restrict__ nmoved,
+                                const T *__restrict__ tmp, const int *__restrict__ tmp_perm,
+                                int *__restrict__ rowperm, T *__restrict__ B)
 {
     const int m = *nmoved;
     const T zero = from_acc<T>(0), one = from_acc<T>(1);
-    // rows: blockIdx.y indexes rows 0..n-1
-    for (long i = blockIdx.y; i < n; i += gridDim.y) {
-        int local = (int)i - k;
+    const int ty = blockIdx.y;
+    const int cx = blockIdx.x * blockDim.x + threadIdx.x, sx = gridDim.x * blockDim.x;
+    if (ty < b) {                                        // block row: B column, then zero
+        const int local = ty;
+        if (local >= n - k) return;
+        const long i = k + local;
         int slot = -1;
-        if (local >= 0 && local < n - k)
-            for (int t = 0; t < m; t++) if (moved[2 * t] == local) { slot = t; break; }
-        const bool in_block = (local >= 0 && local < b);
-        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+        for (int t = 0; t < m; t++) if (moved[2 * t] == local) { slot = t; break; }
+        for (int c = c0 + cx; c < c1; c += sx) {
             const bool panel_col = (c >= k && c < k + b);
-            if (in_block) {
-                T v = (slot >= 0) ? tmp[(long)slot * n + c] : A[i * n + c];
-                B[(long)c * b + local] = panel_col ? ((c - k == local) ? one : zero) : v;   // Bt: n x b
-                A[i * n + c] = zero;
-            } else if (slot >= 0) {
-                A[i * n + c] = panel_col ? zero : tmp[(long)slot * n + c];
-            } else if (panel_col) {
-                A[i * n + c] = zero;
+            const T v = (slot >= 0) ? tmp[(long)slot * n + c] : A[i * n + c];
+            B[(long)c * b + local] = panel_col ? ((c - k == local) ? one : zero) : v;   // Bt: n x b
+            A[i * n + c] = zero;
+        }
+        if (slot >= 0 && cx == 0) rowperm[i] = tmp_perm[slot];
+    } else if (ty < 3 * b) {                             // moved row below the block
+        const int t = ty - b;
+        if (t >= m) return;
+        const int local = moved[2 * t];
+        if (local < b) return;
+        const long i = k + local;
+        for (int c = c0 + cx; c < c1; c += sx) {
+            const bool panel_col = (c >= k && c < k + b);
+            A[i * n + c] = panel_col ? zero : tmp[(long)t * n + c];
+        }
+        if (cx == 0) rowperm[i] = tmp_perm[t];
+    } else {                                             // panel columns of the other rows
+        const long tot = (long)n * b;
+        const long stride = (long)(gridDim.y - 3 * b) * sx;
+        for (long e = (long)(ty - 3 * b) * sx + cx; e < tot; e += stride) {
+            const long i = e / b;
+            const int c = (int)(e - i * b);
+            if (i >= k && i < k + b) continue;
+            A[i * n + k + c] = zero;
+        }
+    }
+}
+
+// Two-level scheme, outer step for the block columns [K0, K0+nb): the inner steps
+// transformed only the block columns; the other columns ("rest") now receive the
+// block's row interchanges (the composite of the transpositions ipiv[K0..K0+nb) in
+// order), then B_outer = the pivot rows' rest entries (n x nb, K-major for the GEMM)
+// and the pivot rows' rest entries are zeroed.
+// (1) one warp: composite permutation of the touched positions -> (dst, src) list
+__global__ void gje_outer_perm_kernel(int K0, int nb, const int *__restrict__ ipiv, int *__restrict__ omoved,
+                                      int *__restrict__ onmoved)
+{
+    __shared__ int cand[2 * GJE_NB], src[2 * GJE_NB];
+    __shared__ int ncand;
+    const int ln = threadIdx.x;
+    for (int t = ln; t < nb; t += 32) { cand[t] = K0 + t; src[t] = K0 + t; }
+    if (ln == 0) ncand = nb;
+    __syncwarp();
+    for (int j = 0; j < nb; j++) {
+        const int pj = ipiv[K0 + j];
+        const int nc0 = ncand;
+        int ip = -1;
+        for (int t0 = 0; t0 < nc0 && ip < 0; t0 += 32) {
+            const unsigned hit = __ballot_sync(0xffffffffu, t0 + ln < nc0 && cand[t0 + ln] == pj);
+            if (hit) ip = t0 + __ffs(hit) - 1;
+        }
+        if (ip < 0) {
+            ip = nc0;
+            if (ln == 0) { cand[ip] = pj; src[ip] = pj; ncand = nc0 + 1; }
+        }
+        __syncwarp();
+        if (ln == 0) { const int t = src[j]; src[j] = src[ip]; src[ip] = t; }
+        __syncwarp();
+    }
+    if (ln == 0) {
+        int m = 0;
+        for (int t = 0; t < ncand; t++)
+            if (src[t] != cand[t]) { omoved[2 * m] = cand[t]; omoved[2 * m + 1] = src[t]; m++; }
+        *onmoved = m;
+    }
+}
+
+// (2) gather the moved source rows' rest entries
+template <typename T>
+__global__ void gje_outer_gather_kernel(int n, int K0, int nb, const T *__restrict__ A, const int *__restrict__ omoved,
+                                        const int *__restrict__ onmoved, T *__restrict__ tmp2)
+{
+    const int t = blockIdx.y;
+    if (t >= *onmoved) return;
+    const long src = omoved[2 * t + 1];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n - nb; e += gridDim.x * blockDim.x) {
+        const int c = e < K0 ? e : e + nb;
+        tmp2[(long)t * n + c] = A[src * n + c];
+    }
+}
+
+// (3) scatter moved rows below the block; pivot rows -> B_outer (transposed through
+// shared memory so both sides are coalesced) and zero
+template <typename T>
+__global__ void __launch_bounds__(256)
+gje_outer_scatter_kernel(int n, int K0, int nb, T *__restrict__ A, const int *__restrict__ omoved,
+                         const int *__restrict__ onmoved, const T *__restrict__ tmp2, T *__restrict__ Bo)
+{
+    const int m = *onmoved;
+    const int nrest = n - nb;
+    if (blockIdx.y == 0) {
+        // pivot rows: tile of 32 rest columns x nb rows
+        __shared__ T tile[32][33];
+        __shared__ int slot[GJE_NB];
+        for (int y = threadIdx.x; y < nb; y += blockDim.x) {
+            int sl = -1;
+            for (int t = 0; t < m; t++) if (omoved[2 * t] == K0 + y) { sl = t; break; }
+            slot[y] = sl;
+        }
+        __syncthreads();
+        const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;     // 32 x 8
+        for (int e0 = blockIdx.x * 32; e0 < nrest; e0 += gridDim.x * 32) {
+            for (int y0 = 0; y0 < nb; y0 += 32) {
+                for (int yy = ty; yy < 32; yy += 8) {
+                    const int y = y0 + yy, e = e0 + tx;
+                    T v = from_acc<T>(0);
+                    if (y < nb && e < nrest) {
+                        const int c = e < K0 ? e : e + nb;
+                        const long row = K0 + y;
+                        v = slot[y] >= 0 ? tmp2[(long)slot[y] * n + c] : A[row * n + c];
+                        A[row * n + c] = from_acc<T>(0);
+                    }
+                    tile[yy][tx] = v;
+                }
+                __syncthreads();
+                for (int cc = ty; cc < 32; cc += 8) {
+                    const int e = e0 + cc, y = y0 + tx;
+                    if (e < nrest && y < nb) {
+                        const int c = e < K0 ? e : e + nb;
+                        Bo[(long)c * nb + y] = tile[tx][cc];
+                    }
+                }
+                __syncthreads();
             }
         }
-        if (slot >= 0 && blockIdx.x == 0 && threadIdx.x == 0) rowperm[i] = tmp_perm[slot];
+    } else {
+        const int t = blockIdx.y - 1;
+        if (t >= m) return;
+        const int dst = omoved[2 * t];
+        if (dst < K0 + nb) return;                               // pivot rows handled above
+        for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nrest; e += gridDim.x * blockDim.x) {
+            const int c = e < K0 ? e : e + nb;
+            A[(long)dst * n + c] = tmp2[(long)t * n + c];
+        }
     }
 }
 
@@ -261,6 +616,13 @@ int GjeWork::alloc(int n_, int prec_) {
     LYAP_CUDA_TRY(cudaMalloc(&B, es * (size_t)n * b));
     LYAP_CUDA_TRY(cudaMalloc(&tmp, es * (size_t)n * 2 * b));
     LYAP_CUDA_TRY(cudaMalloc(&Pglob, acc * (size_t)n * b));
+    LYAP_CUDA_TRY(cudaMalloc(&Tg, acc * 32 * 32));
+    if ((prec == LYAP_FP16 || prec == LYAP_BF16) && n % 8 == 0 && n >= 2 * GJE_NB) {
+        LYAP_CUDA_TRY(cudaMalloc(&Bo, es * (size_t)n * GJE_NB));
+        LYAP_CUDA_TRY(cudaMalloc(&tmp2, es * (size_t)n * 2 * GJE_NB));
+        LYAP_CUDA_TRY(cudaMalloc(&oints, sizeof(int) * (4 * GJE_NB + 4)));
+        omoved = oints; onmoved = oints + 4 * GJE_NB;
+    }
     LYAP_CUDA_TRY(cudaMalloc(&ints, sizeof(int) * (size_t)(4 * n + 4 * b + 8)));
     ipiv = ints; rowperm = ipiv + n; invperm = rowperm + n; moved = invperm + n;
     nmoved = moved + 4 * b; info = nmoved + 1; tmp_perm = info + 1;
@@ -268,8 +630,83 @@ int GjeWork::alloc(int n_, int prec_) {
 }
 
 void GjeWork::release() {
-    cudaFree(X); cudaFree(B); cudaFree(tmp); cudaFree(Pglob); cudaFree(ints);
-    X = B = tmp = nullptr; Pglob = nullptr; ints = nullptr;
+    cudaFree(X); cudaFree(B); cudaFree(tmp); cudaFree(Pglob); cudaFree(Tg); cudaFree(Bo); cudaFree(tmp2);
+    cudaFree(ints); cudaFree(oints);
+    X = B = tmp = nullptr; Pglob = Tg = Bo = tmp2 = nullptr; ints = oints = omoved = onmoved = nullptr;
+}
+
+// X rows above the panel: X[i, :] = -A[i, k:k+b] T for i < k.  One warp per row: the
+// row's b panel entries are read once (coalesced) and broadcast by shuffles; same
+// summation order as the single-CTA kernel.
+template <typename T>
+__global__ void __launch_bounds__(256)
+gje_xabove_kernel(int n, int k, int b, const T *__restrict__ A, const typename Prec<T>::acc *__restrict__ Tglob,
+                  T *__restrict__ X)
+{
+    using Acc = typename Prec<T>::acc;
+    __shared__ Acc Ts[32 * 32];
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) Ts[e] = Tglob[e];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < k; i += gridDim.x * 8) {
+        const Acc a = lane < b ? to_acc<T>(A[(long)i * n + k + lane]) : Acc(0);
+        Acc sacc = Acc(0);
+        for (int t = 0; t < b; t++) sacc = fma(-__shfl_sync(0xffffffffu, a, t), Ts[t * 32 + lane], sacc);
+        if (lane < b) X[(long)i * b + lane] = from_acc<T>(sacc);
+    }
+}
+
+// panel rows per CTA and cluster size: about 512 rows per CTA (one per thread), at
+// least b rows on CTA 0, up to 16 CTAs (non-portable cluster size) for tall panels
+template <typename T>
+static int gje_panel_launch(cudaStream_t s, int n, int k, int b, T *A, GjeWork &w)
+{
+    using Acc = typename Prec<T>::acc;
+    constexpr int BW = std::is_same<T, double>::value ? 16 : 32;
+    const int R = n - k;
+    int nc = std::max(1, std::min(16, ceil_div(R, 512)));
+    if (const char *e = getenv("LYAP_GJE_NC")) nc = std::max(1, std::min(16, atoi(e)));
+    const int RB = std::max(b, ceil_div(R, nc));
+    nc = ceil_div(R, RB);
+    if (RB > 2 * 512 || b > BW || env_flag("LYAP_GJE_1CTA")) {
+        bool use_smem;
+        size_t sm = gje_panel_smem(n, Prec<T>::code, b, R, &use_smem);
+        static bool attr1 = false;
+        if (!attr1) {
+            LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            attr1 = true;
+        }
+        gje_panel_kernel<T><<<1, 1024, sm, s>>>(n, k, b, A, (T *)w.X, w.ipiv, w.moved, w.nmoved, w.info,
+                                                (Acc *)w.Pglob, use_smem ? 1 : 0);
+        return launched();
+    }
+    auto kern = (RB > 512) ? gje_panel_cluster_kernel<T, BW, 2> : gje_panel_cluster_kernel<T, BW, 1>;
+    static bool attr = false;
+    if (!attr) {
+        LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nc, 1, 1);
+    cfg.blockDim = dim3(512, 1, 1);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = nc;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    LYAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, n, k, b, RB, (const T *)A, (T *)w.X, w.ipiv, w.moved, w.nmoved,
+                                     w.info, (Acc *)w.Tg));
+    LYAP_TRY(launched());
+    if (k > 0) {
+        gje_xabove_kernel<T><<<std::min(ceil_div(k, 8), 1184), 256, 0, s>>>(n, k, b, (const T *)A, (const Acc *)w.Tg,
+                                                                          (T *)w.X);
+    }
+    return launched();
 }
 
 template <typename T>
@@ -280,31 +717,56 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
     LYAP_CUDA_TRY(cudaMemsetAsync(w.info, 0, sizeof(int), s));
     iota_kernel<<<ceil_div(n, 256), 256, 0, s>>>(n, w.rowperm);
     LYAP_TRY(launched());
-    for (int k = 0; k < n; k += b0) {
-        int b = (n - k < b0) ? n - k : b0;
-        bool use_smem;
-        size_t sm = gje_panel_smem(n, Prec<T>::code, b, n - k, &use_smem);
-        static bool attr_set = false;
-        if (!attr_set) {
-            LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-            attr_set = true;
+    // two-level blocking for the 16-bit types: inner 32-wide steps restricted to an
+    // outer block of NB columns, then one rank-NB tensor-core update of the rest
+    constexpr bool half_t = std::is_same<T, __half>::value || std::is_same<T, __nv_bfloat16>::value;
+    const bool two_level = half_t && !use_simt_gemm() && n % 8 == 0 && n >= 2 * GJE_NB && w.Bo != nullptr &&
+                           !env_flag("LYAP_GJE_1LEVEL");
+    const int NBo = two_level ? GJE_NB : n;
+    for (int K0 = 0; K0 < n; K0 += NBo) {
+        const int nbk = std::min(NBo, n - K0);
+        const int c0 = two_level ? K0 : 0, c1 = two_level ? K0 + nbk : n;
+        for (int k = K0; k < K0 + nbk; k += b0) {
+            const int b = std::min(b0, K0 + nbk - k);
+            {
+                KTimer kt(KC_GJE_PANEL, s);
+                LYAP_TRY(gje_panel_launch<T>(s, n, k, b, A, w));
+            }
+            LYAP_TRY(launched());
+            dim3 gg(ceil_div(c1 - c0, 256) < 8 ? ceil_div(c1 - c0, 256) : 8, 2 * b);
+            gje_gather_kernel<T><<<gg, 256, 0, s>>>(n, k, A, w.moved, w.nmoved, (T *)w.tmp, w.rowperm, w.tmp_perm);
+            LYAP_TRY(launched());
+            dim3 gp(std::min(ceil_div(c1 - c0, 256), 8), 3 * b + std::min(ceil_div((long)n * b, 8 * 256), 512));
+            gje_prep_kernel<T><<<gp, 256, 0, s>>>(n, k, b, c0, c1, A, w.moved, w.nmoved, (const T *)w.tmp,
+                                                  w.tmp_perm, w.rowperm, (T *)w.B);
+            LYAP_TRY(launched());
+            {
+                KTimer kt(KC_GJE_UPDATE, s);
+                if (two_level)
+                    LYAP_TRY(tc_gemm(s, Prec<T>::code, n, nbk, b, 1.0f, w.X, b, (const T *)w.B + (size_t)K0 * b, b,
+                                     1.0f, A + K0, n, 0));
+                else
+                    LYAP_TRY(gemm_update(s, n, b, (const T *)w.X, (const T *)w.B, A));
+            }
         }
-        {
-            KTimer kt(KC_GJE_PANEL, s);
-            gje_panel_kernel<T><<<1, 1024, sm, s>>>(n, k, b, A, (T *)w.X, w.ipiv + 0, w.moved, w.nmoved,
-                                                    w.info, (Acc *)w.Pglob, use_smem ? 1 : 0);
-        }
-        LYAP_TRY(launched());
-        dim3 gg(ceil_div(n, 256) < 8 ? ceil_div(n, 256) : 8, 2 * b);
-        gje_gather_kernel<T><<<gg, 256, 0, s>>>(n, k, A, w.moved, w.nmoved, (T *)w.tmp, w.rowperm, w.tmp_perm);
-        LYAP_TRY(launched());
-        dim3 gp(ceil_div(n, 256) < 4 ? ceil_div(n, 256) : 4, n < 4096 ? n : 4096);
-        gje_prep_kernel<T><<<gp, 256, 0, s>>>(n, k, b, A, w.moved, w.nmoved, (const T *)w.tmp, w.tmp_perm,
-                                              w.rowperm, (T *)w.B);
-        LYAP_TRY(launched());
-        {
+        if (two_level && n - nbk > 0) {
+            gje_outer_perm_kernel<<<1, 32, 0, s>>>(K0, nbk, w.ipiv, w.omoved, w.onmoved);
+            LYAP_TRY(launched());
+            const int gx = std::min(ceil_div(n - nbk, 256), 64);
+            gje_outer_gather_kernel<T><<<dim3(gx, 2 * nbk), 256, 0, s>>>(n, K0, nbk, A, w.omoved, w.onmoved,
+                                                                       (T *)w.tmp2);
+            LYAP_TRY(launched());
+            gje_outer_scatter_kernel<T><<<dim3(std::min(ceil_div(n - nbk, 32), 592), 1 + 2 * nbk), 256, 0, s>>>(
+                n, K0, nbk, A, w.omoved, w.onmoved, (const T *)w.tmp2, (T *)w.Bo);
+            LYAP_TRY(launched());
             KTimer kt(KC_GJE_UPDATE, s);
-            LYAP_TRY(gemm_update(s, n, b, (const T *)w.X, (const T *)w.B, A));
+            // A[:, rest] += X_outer B_outer, X_outer = the block columns (ld n)
+            if (K0 > 0)
+                LYAP_TRY(tc_gemm(s, Prec<T>::code, n, K0, nbk, 1.0f, A + K0, n, (const T *)w.Bo, nbk, 1.0f, A, n, 0));
+            const int cr = K0 + nbk;
+            if (cr < n)
+                LYAP_TRY(tc_gemm(s, Prec<T>::code, n, n - cr, nbk, 1.0f, A + K0, n, (const T *)w.Bo + (size_t)cr * nbk,
+                                 nbk, 1.0f, A + cr, n, 0));
         }
     }
     invperm_kernel<<<ceil_div(n, 256), 256, 0, s>>>(n, w.rowperm, w.invperm);

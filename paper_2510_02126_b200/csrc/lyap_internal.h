@@ -6,9 +6,11 @@
 namespace lyap {
 
 // Workspace of the blocked Gauss-Jordan inversion (gje.cu).
+constexpr int GJE_NB = 256;       // outer block of the two-level Gauss-Jordan scheme (16-bit types)
 struct GjeWork {
     int n = 0, prec = 0;
-    void *X = nullptr, *B = nullptr, *tmp = nullptr, *Pglob = nullptr;
+    void *X = nullptr, *B = nullptr, *tmp = nullptr, *Pglob = nullptr, *Tg = nullptr, *Bo = nullptr, *tmp2 = nullptr;
+    int *oints = nullptr, *omoved = nullptr, *onmoved = nullptr;
     int *ints = nullptr;
     int *ipiv = nullptr, *rowperm = nullptr, *invperm = nullptr, *moved = nullptr;
     int *nmoved = nullptr, *info = nullptr, *tmp_perm = nullptr;

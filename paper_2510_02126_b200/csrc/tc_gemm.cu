@@ -13,7 +13,8 @@
 //                              N=128, K=16) into a 128-column fp32 TMEM accumulator,
 //                              tcgen05.commit releases each smem stage;
 //   warps 0-3                  epilogue: tcgen05.ld 32x32b (each thread one row),
-//                              alpha/beta blend with C, 16-bit store.
+//                              alpha/beta blend with C staged through the idle
+//                              pipeline shared memory, row-coalesced 16-bit stores.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include "common.cuh"
@@ -25,7 +26,12 @@ namespace lyap {
 namespace tc {
 constexpr int BM = 128, BN = 128, BK = 64, STAGES = 4;
 constexpr int A_STAGE = BM * BK * 2, B_STAGE = BN * BK * 2;          // bytes
-constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) + 1024 + 256;     // + alignment + barriers
+constexpr int C_STAGE = BM * BN * 2;                                 // C tile (TMA epilogue)
+constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) + C_STAGE + 1024 + 256;   // + alignment + barriers
+// pipeline depth by K: short-K updates (the Gauss-Jordan rank-b steps) keep the
+// shared-memory footprint small so 2-3 CTAs share an SM and overlap their epilogues
+__host__ __device__ constexpr int smem_bytes(int ns) { return ns * (A_STAGE + B_STAGE) + C_STAGE + 1024 + 256; }
+inline int stages_for(int nk) { return nk <= 2 ? nk : (nk <= 4 ? 2 : STAGES); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -48,6 +54,10 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
         :: "r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, const void *src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+                 :: "l"(map), "r"(smem_u32(src)), "r"(c0), "r"(c1) : "memory");
 }
 // K-major, 128B-swizzled canonical layout: 8-row x 128-byte atoms, atoms 1024 B apart.
 __device__ __forceinline__ uint64_t smem_desc(const void *p) {
@@ -80,26 +90,30 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float *v) {
 }  // namespace tc
 
 template <typename T>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(128, 3)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               int M, int N, int K, float alpha, float beta, T *__restrict__ C, long ldc, int colmajor)
+               const __grid_constant__ CUtensorMap tmC, int M, int N, int K, float alpha, float beta,
+               T *__restrict__ C, long ldc, int colmajor, int ctma, int ns)
 {
     using namespace tc;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *base = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *sA = base;
-    unsigned char *sB = base + STAGES * A_STAGE;
-    uint64_t *full = (uint64_t *)(sB + STAGES * B_STAGE);
-    uint64_t *empty = full + STAGES;
-    uint64_t *done = empty + STAGES;
-    uint32_t *tmem_slot = (uint32_t *)(done + 1);
+    unsigned char *sB = base + ns * A_STAGE;
+    unsigned char *sC = sB + ns * B_STAGE;                  // 1024-aligned (stage sizes are)
+    uint64_t *full = (uint64_t *)(sC + C_STAGE);
+    uint64_t *empty = full + ns;
+    uint64_t *done = empty + ns;
+    uint64_t *cbar = done + 1;
+    uint32_t *tmem_slot = (uint32_t *)(cbar + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
     const int nk = (K + BK - 1) / BK;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        for (int s = 0; s < ns; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
         tc::mbar_init(done, 1);
+        tc::mbar_init(cbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" :: "l"(&tmA) : "memory");
         asm volatile("prefetch.tensormap [%0];" :: "l"(&tmB) : "memory");
@@ -115,10 +129,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0 && lane == 0) {
-        // ---------------- TMA producer
+        // ---------------- TMA producer (the C tile first when it is blended in)
+        if (ctma && beta != 0.f) {
+            tc::mbar_expect_tx(cbar, C_STAGE);
+            for (int w = 0; w < 4; w++)
+                for (int hh = 0; hh < 2; hh++)
+                    tc::tma_load_2d(sC + (w * 2 + hh) * 4096, &tmC, cbar, n0 + 64 * hh, m0 + 32 * w);
+        }
         for (int kb = 0; kb < nk; kb++) {
-            const int s = kb % STAGES;
-            if (kb >= STAGES) tc::mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+            const int s = kb % ns;
+            if (kb >= ns) tc::mbar_wait(&empty[s], ((kb / ns) - 1) & 1);
             tc::mbar_expect_tx(&full[s], A_STAGE + B_STAGE);
             tc::tma_load_2d(sA + s * A_STAGE, &tmA, &full[s], kb * BK, m0);
             tc::tma_load_2d(sB + s * B_STAGE, &tmB, &full[s], kb * BK, n0);
@@ -129,8 +149,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
                                ((uint32_t)(BM >> 4) << 24);
         for (int kb = 0; kb < nk; kb++) {
-            const int s = kb % STAGES;
-            tc::mbar_wait(&full[s], (kb / STAGES) & 1);
+            const int s = kb % ns;
+            tc::mbar_wait(&full[s], (kb / ns) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint64_t da = tc::smem_desc(sA + s * A_STAGE), db = tc::smem_desc(sB + s * B_STAGE);
 #pragma unroll
@@ -144,18 +164,75 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     tc::mbar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
     const int row = m0 + warp * 32 + lane;
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-        if (row < M) {
+    if (colmajor) {
+        // consecutive lanes = consecutive rows = consecutive addresses: coalesced as is
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+            float v[16];
+            tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+            if (row < M) {
 #pragma unroll
-            for (int i = 0; i < 16; i++) {
-                const int col = n0 + c0 + i;
-                if (col < N) {
-                    T *cp = colmajor ? C + (long)col * ldc + row : C + (long)row * ldc + col;
-                    float r = alpha * v[i];
-                    if (beta != 0.f) r = fmaf(beta, to_f<T>(*cp), r);
-                    *cp = from_f<T>(r);
+                for (int i = 0; i < 16; i++) {
+                    const int col = n0 + c0 + i;
+                    if (col < N) {
+                        T *cp = C + (long)col * ldc + row;
+                        float r = alpha * v[i];
+                        if (beta != 0.f) r = fmaf(beta, to_f<T>(*cp), r);
+                        *cp = from_f<T>(r);
+                    }
+                }
+            }
+        }
+    } else if (ctma) {
+        // row-major C through TMA: the warp's 32 x 128 tile is two 32 x 64 boxes in
+        // 128B-swizzled shared memory (16-byte chunk j of row r at chunk j ^ (r & 7)),
+        // loaded by the producer before the main loop and stored back by TMA.
+        if (beta != 0.f) tc::mbar_wait(cbar, 0);
+        unsigned char *wbox = sC + warp * 2 * 4096;
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+            float v[16];
+            tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+            unsigned char *rowp = wbox + (c0 >> 6) * 4096 + lane * 128;
+            const int j0 = (c0 & 63) >> 3;
+            uint4 *p0 = reinterpret_cast<uint4 *>(rowp + (((j0) ^ (lane & 7)) << 4));
+            uint4 *p1 = reinterpret_cast<uint4 *>(rowp + (((j0 + 1) ^ (lane & 7)) << 4));
+            alignas(16) T o[16];
+            if (beta != 0.f) {
+                alignas(16) T ci[16];
+                *reinterpret_cast<uint4 *>(ci) = *p0;
+                *reinterpret_cast<uint4 *>(ci + 8) = *p1;
+#pragma unroll
+                for (int i = 0; i < 16; i++) o[i] = from_f<T>(fmaf(beta, to_f<T>(ci[i]), alpha * v[i]));
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; i++) o[i] = from_f<T>(alpha * v[i]);
+            }
+            *p0 = *reinterpret_cast<const uint4 *>(o);
+            *p1 = *reinterpret_cast<const uint4 *>(o + 8);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            tc::tma_store_2d(&tmC, wbox, n0, m0 + 32 * warp);
+            tc::tma_store_2d(&tmC, wbox + 4096, n0 + 64, m0 + 32 * warp);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        __syncwarp();
+    } else {
+        // generic row-major fallback (unaligned C): one element per access
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+            float v[16];
+            tc::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+            if (row < M) {
+#pragma unroll
+                for (int i = 0; i < 16; i++) {
+                    const int col = n0 + c0 + i;
+                    if (col < N) {
+                        T *cp = C + (long)row * ldc + col;
+                        float r = alpha * v[i];
+                        if (beta != 0.f) r = fmaf(beta, to_f<T>(*cp), r);
+                        *cp = from_f<T>(r);
+                    }
                 }
             }
         }
@@ -192,7 +269,7 @@ int make_map(CUtensorMap *m, const void *ptr, int prec, long rows, long cols, lo
     CUresult r = fn(m, prec == LYAP_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
                     const_cast<void *>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);      // out-of-bounds elements read as zero
     return r == CUDA_SUCCESS ? LYAP_OK : LYAP_ERR_ARG;
 }
 }  // namespace
@@ -204,10 +281,17 @@ int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const vo
     if (M <= 0 || N <= 0 || K <= 0) return LYAP_OK;
     if (prec != LYAP_BF16 && prec != LYAP_FP16) return LYAP_ERR_ARG;
     if ((lda * 2) % 16 || (ldb * 2) % 16 || ((uintptr_t)A % 16) || ((uintptr_t)B % 16)) return LYAP_ERR_ARG;
-    CUtensorMap ma, mb;
+    CUtensorMap ma, mb, mc;
     LYAP_TRY(make_map(&ma, A, prec, M, K, lda, tc::BM));
     LYAP_TRY(make_map(&mb, B, prec, N, K, ldb, tc::BN));
+    // TMA epilogue for row-major C with 16-byte aligned rows
+    const int ctma = (!colmajor && (ldc * 2) % 16 == 0 && ((uintptr_t)C % 16) == 0 && !env_flag("LYAP_TC_NO_CTMA"))
+                         ? 1 : 0;
+    if (ctma) LYAP_TRY(make_map(&mc, C, prec, M, N, ldc, 32));
+    else mc = ma;
     dim3 grid(ceil_div(N, tc::BN), ceil_div(M, tc::BM));
+    const int ns = tc::stages_for(ceil_div(K, tc::BK));
+    const int smem = tc::smem_bytes(ns);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(tc_gemm_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM);
@@ -216,10 +300,11 @@ int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const vo
     }
     KTimer kt(KC_TCGEMM, s, 2.0 * M * N * K, 2.0 * ((double)M * K + (double)N * K + (beta != 0.f ? 2.0 : 1.0) * M * N));
     if (prec == LYAP_BF16)
-        tc_gemm_kernel<__nv_bfloat16><<<grid, 128, tc::SMEM, s>>>(ma, mb, M, N, K, alpha, beta, (__nv_bfloat16 *)C,
-                                                                   ldc, colmajor);
+        tc_gemm_kernel<__nv_bfloat16><<<grid, 128, smem, s>>>(ma, mb, mc, M, N, K, alpha, beta,
+                                                               (__nv_bfloat16 *)C, ldc, colmajor, ctma, ns);
     else
-        tc_gemm_kernel<__half><<<grid, 128, tc::SMEM, s>>>(ma, mb, M, N, K, alpha, beta, (__half *)C, ldc, colmajor);
+        tc_gemm_kernel<__half><<<grid, 128, smem, s>>>(ma, mb, mc, M, N, K, alpha, beta, (__half *)C, ldc,
+                                                       colmajor, ctma, ns);
     return launched();
 }
 

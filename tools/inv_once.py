@@ -1,0 +1,8 @@
+"""One u_s inversion at size n (for ncu launch lists)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2510_02126_b200 as G
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+A = (torch.randn(n, n, device="cuda") / n ** 0.5 - 2 * torch.eye(n, device="cuda")).to(torch.bfloat16)
+G.invert(A); torch.cuda.synchronize()
