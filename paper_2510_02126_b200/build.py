@@ -34,7 +34,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [NVCC] + FLAGS + ["-c", src, "-o", obj]
+        extra = os.environ.get("LYAP_NVCC_EXTRA", "").split()      # e.g. -DLYAP_PANEL_PROF (instrumented builds)
+        cmd = [NVCC] + FLAGS + extra + ["-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     for src, p in procs:
         out, _ = p.communicate()

@@ -196,6 +196,60 @@ __device__ __forceinline__ Acc sel_col(const Acc (&r)[BW], int j) {
     return v;
 }
 
+// Warp argmax of (v >= 0 or -1 for "none", index), ties to the lower index, result in
+// every lane.  Candidates must be ordered: lane order = index order among equal values
+// (callers guarantee it).  fp32: one redux.sync max over the value bits + a ballot;
+// fp64: butterfly of (value, index) pairs.
+template <typename Acc>
+__device__ __forceinline__ void warp_argmax(Acc &v, int &i, int lane) {
+    if constexpr (sizeof(Acc) == 4) {
+        // key 0 = no candidate / NaN (never selected, as in argmax_merge), else bits + 1
+        const unsigned key = (v >= 0.f) ? __float_as_uint(v) + 1u : 0u;
+        const unsigned mx = __reduce_max_sync(0xffffffffu, key);
+        const unsigned who = __ballot_sync(0xffffffffu, key == mx);
+        const int src = __ffs(who) - 1;
+        v = __shfl_sync(0xffffffffu, v, src);
+        i = __shfl_sync(0xffffffffu, i, src);
+        if (mx == 0u) v = Acc(-1);
+    } else {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            Acc v2 = __shfl_xor_sync(0xffffffffu, v, o);
+            int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+            argmax_merge(v, i, v2, i2);
+        }
+    }
+    (void)lane;
+}
+
+// a register row to / from 16-byte aligned shared memory, vectorised
+template <typename Acc, int BW>
+__device__ __forceinline__ void row_store(const Acc (&r)[BW], Acc *dst) {
+    if constexpr (sizeof(Acc) == 4) {
+#pragma unroll
+        for (int c = 0; c < BW; c += 4) *reinterpret_cast<float4 *>(dst + c) = make_float4(r[c], r[c + 1], r[c + 2], r[c + 3]);
+    } else {
+#pragma unroll
+        for (int c = 0; c < BW; c += 2) *reinterpret_cast<double2 *>(dst + c) = make_double2(r[c], r[c + 1]);
+    }
+}
+template <typename Acc, int BW>
+__device__ __forceinline__ void row_load(Acc (&r)[BW], const Acc *src) {
+    if constexpr (sizeof(Acc) == 4) {
+#pragma unroll
+        for (int c = 0; c < BW; c += 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(src + c);
+            r[c] = v.x; r[c + 1] = v.y; r[c + 2] = v.z; r[c + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < BW; c += 2) {
+            const double2 v = *reinterpret_cast<const double2 *>(src + c);
+            r[c] = v.x; r[c + 1] = v.y;
+        }
+    }
+}
+
 template <typename T, int BW, int RPT>
 __global__ void __launch_bounds__(512)
 gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T *__restrict__ X,
@@ -210,9 +264,9 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int R = n - k;
     const int g0 = q * RB, nloc = max(0, min(RB, R - g0));
-    constexpr int PW = 2 + 2 * BW;                             // |cand|, row index, cand row, row j
-    __shared__ Acc pub[2][PW];
-    __shared__ Acc inbox[2][16][PW];                           // pushed by every CTA of the cluster
+    constexpr int PW = 2 * BW + 4;                             // cand row, row j, |cand|, row index (16B-aligned rows)
+    __shared__ __align__(16) Acc pub[2][PW];
+    __shared__ __align__(16) Acc inbox[2][16][PW];             // pushed by every CTA of the cluster
     __shared__ Acc redv[16];
     __shared__ int redi[16];
     __shared__ int pivl[32];
@@ -222,96 +276,103 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
     Acc row[RPT][BW];
 #pragma unroll
     for (int h = 0; h < RPT; h++) {
-        const int r = tid + NT * h;
+        const int r = RPT * tid + h;
         const T *src = A + (long)(k + g0 + r) * n + k;
 #pragma unroll
         for (int c = 0; c < BW; c++) row[h][c] = (r < nloc && c < b) ? to_acc<T>(src[c]) : Acc(0);
     }
     if (tid == 0) sflag = 0;
+#ifdef LYAP_PANEL_PROF
+    long long pt[6] = {0, 0, 0, 0, 0, 0}, tl = clock64();
+#define PPROF(i) do { if (q == 0 && tid == 0) { long long t_ = clock64(); pt[i] += t_ - tl; tl = t_; } } while (0)
+#else
+#define PPROF(i) do { } while (0)
+#endif
     // columns unrolled: every register index and every (c > j) test is a compile-time constant
 #pragma unroll
     for (int j = 0; j < BW; j++) {
         if (j >= b) break;
         const int buf = j & 1;
-        // ---- local candidate: max |P[r][j]|, panel row >= j, lowest row on ties
+        // ---- local candidate: max |P[r][j]|, panel row >= j, lowest row on ties.  Rows
+        // increase with (thread, slot), warp and CTA, so "lowest slot holding the maximum"
+        // is the lowest row (the single-CTA tie rule).
         Acc bv = Acc(-1); int bi = R;
 #pragma unroll
         for (int h = 0; h < RPT; h++) {
-            const int r = tid + NT * h, gi = g0 + r;
+            const int r = RPT * tid + h, gi = g0 + r;
             if (r < nloc && gi >= j) argmax_merge(bv, bi, fabs(row[h][j]), gi);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            Acc v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-            int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-            argmax_merge(bv, bi, v2, i2);
-        }
+        warp_argmax<Acc>(bv, bi, lane);
         if (lane == 0) { redv[wid] = bv; redi[wid] = bi; }
+        PPROF(0);
         __syncthreads();
+        PPROF(1);
         bv = lane < 16 ? redv[lane] : Acc(-1);
         bi = lane < 16 ? redi[lane] : R;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {                     // every lane needs the CTA winner
-            Acc v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-            int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-            argmax_merge(bv, bi, v2, i2);
-        }
-        if (tid == 0) { pub[buf][0] = bv; pub[buf][1] = Acc(bi); }
+        warp_argmax<Acc>(bv, bi, lane);                        // every lane needs the CTA winner
+        if (tid == 0) { pub[buf][2 * BW] = bv; pub[buf][2 * BW + 1] = Acc(bi); }
 #pragma unroll
         for (int h = 0; h < RPT; h++) {
-            const int r = tid + NT * h, gi = g0 + r;
-            if (r < nloc && gi == bi)
-#pragma unroll
-                for (int c = 0; c < BW; c++) pub[buf][2 + c] = row[h][c];
-            if (r < nloc && gi == j)
-#pragma unroll
-                for (int c = 0; c < BW; c++) pub[buf][2 + BW + c] = row[h][c];
+            const int r = RPT * tid + h, gi = g0 + r;
+            const bool own_c = r < nloc && gi == bi, own_j = r < nloc && gi == j;
+            if (__any_sync(0xffffffffu, own_c || own_j)) {            // one warp (or two) per CTA
+                if (own_c) row_store<Acc, BW>(row[h], &pub[buf][0]);
+                if (own_j) row_store<Acc, BW>(row[h], &pub[buf][BW]);
+            }
         }
         __syncthreads();
+        PPROF(2);
         // ---- push this CTA's candidate (and row j) into every CTA's inbox
         if (wid < NC) {
             Acc *dst = cl.map_shared_rank(&inbox[buf][q][0], wid);
             for (int e = lane; e < PW; e += 32) dst[e] = pub[buf][e];
         }
         cl.sync();
-        // ---- global winner from the local inbox, pivot row read as shared-memory broadcasts
+        PPROF(3);
+        // ---- global winner from the local inbox
         Acc gbv = Acc(-1); int gbi = R;
-        for (int w = 0; w < NC; w++) argmax_merge(gbv, gbi, inbox[buf][w][0], (int)inbox[buf][w][1]);
+        if (lane < NC) { gbv = inbox[buf][lane][2 * BW]; gbi = (int)inbox[buf][lane][2 * BW + 1]; }
+        warp_argmax<Acc>(gbv, gbi, lane);
         const int pr = gbi < R ? gbi : j;                      // empty column: no swap (info is set)
-        const Acc *pvp = &inbox[buf][pr / RB][2];
-        const Acc *rjp = &inbox[buf][j / RB][2 + BW];
+        const Acc *pvp = &inbox[buf][pr / RB][0];
+        const Acc *rjp = &inbox[buf][j / RB][BW];
         if (tid == 0) {
             pivl[j] = pr;
             if (!(gbv > Acc(0)) && sflag == 0) sflag = k + j + 1;
         }
         const Acc d = pvp[j];
         const Acc inv = (d != Acc(0)) ? Acc(1) / d : Acc(0);
+        PPROF(4);
 #pragma unroll
         for (int h = 0; h < RPT; h++) {
-            const int r = tid + NT * h, gi = g0 + r;
-            if (r >= nloc) continue;
-            if (gi == j) {
-                if (pr != j)
+            const int r = RPT * tid + h, gi = g0 + r;
+            const bool is_j = r < nloc && gi == j && pr != j, is_p = r < nloc && gi == pr && gi > j;
+            if (__any_sync(0xffffffffu, is_j || is_p)) {
+                if (is_j) row_load<Acc, BW>(row[h], pvp);
+                if (is_p) row_load<Acc, BW>(row[h], rjp);
+            }
+            if (r < nloc && gi > j && d != Acc(0)) {
+                const Acc l = row[h][j] * inv;
+                row[h][j] = l;
 #pragma unroll
-                    for (int c = 0; c < BW; c++) row[h][c] = pvp[c];
-            } else if (gi > j) {
-                if (gi == pr)
-#pragma unroll
-                    for (int c = 0; c < BW; c++) row[h][c] = rjp[c];
-                if (d != Acc(0)) {
-                    const Acc l = row[h][j] * inv;
-                    row[h][j] = l;
-#pragma unroll
-                    for (int c = j + 1; c < BW; c++) row[h][c] = fma(-l, pvp[c], row[h][c]);
-                }
+                for (int c = j + 1; c < BW; c++) row[h][c] = fma(-l, pvp[c], row[h][c]);
             }
         }
+        PPROF(5);
     }
+#ifdef LYAP_PANEL_PROF
+    if (q == 0 && tid == 0 && (k == 0 || k == 2048))
+        printf("panel k=%d R=%d NC=%d cycles/col: argmax %lld bar1 %lld winner+pub+bar2 %lld push+csync %lld "
+               "select %lld elim %lld\n", k, R, NC, pt[0] / b, pt[1] / b, pt[2] / b, pt[3] / b, pt[4] / b, pt[5] / b);
+#endif
     // ---- Linv = L11^{-1}, Uinv = U11^{-1}, T = Uinv Linv on CTA 0 (owns panel rows 0..b-1);
     // same recurrences and summation order as the single-CTA kernel, loops unrolled
-    if (q == 0 && tid < b) {
 #pragma unroll
-        for (int c = 0; c < BW; c++) if (c < b) Ptop[tid][c] = row[0][c];
+    for (int h = 0; h < RPT; h++) {
+        const int r = RPT * tid + h;
+        if (q == 0 && r < b)
+#pragma unroll
+            for (int c = 0; c < BW; c++) if (c < b) Ptop[r][c] = row[h][c];
     }
     __syncthreads();
     if (q == 0) {
@@ -388,7 +449,7 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
     // above the panel split evenly over the cluster
 #pragma unroll
     for (int h = 0; h < RPT; h++) {
-        const int r = tid + NT * h, gi = g0 + r;
+        const int r = RPT * tid + h, gi = g0 + r;
         if (r >= nloc) continue;
         T *xr = X + (long)(k + gi) * b;
         for (int c = 0; c < b; c++) {
