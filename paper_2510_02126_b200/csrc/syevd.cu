@@ -228,6 +228,143 @@ tridiag_reg_kernel(TridArgs a)
     }
 }
 
+// One grid barrier per column and one block barrier: warp 0 of every CTA forms, with
+// warp-level reductions only, the quantities every CTA needs for step j (w = P - k v,
+// column j+1 after step j, the next reflector vn) in shared memory; the owners then
+// update their register-resident columns and publish P[g] = tau_{j+1} (col_g . vn).
+// Same arithmetic as tridiag_reg_kernel up to the reduction trees.
+template <int CH>
+__global__ void __launch_bounds__(256)
+tridiag_w_kernel(TridArgs a)
+{
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sm[];
+    const int p = a.p;
+    double *vb[2] = {sm, sm + p};
+    double *w = sm + 2 * p;
+    __shared__ double s_tau[2], s_beta[2];
+    __shared__ double red1[32], red2[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int g = blockIdx.x * nwb + wid;
+    const bool owner = g < p;
+    double *A = a.A;
+    double col[CH];
+#pragma unroll
+    for (int u = 0; u < CH; u++) {
+        const int i = lane + 32 * u;
+        col[u] = (owner && i < p) ? A[(long)g * p + i] : 0.0;
+    }
+    // reflector 0 from column 0, rows 1.. (warp 0 of every CTA)
+    if (wid == 0) {
+        double ss = 0.0;
+        for (int i = 2 + lane; i < p; i += 32) { const double x = A[i]; ss = fma(x, x, ss); }
+        ss = warp_sum(ss);
+        const double alpha = A[1];
+        double tau = 0.0, beta = alpha;
+        if (ss != 0.0) { beta = -copysign(sqrt(alpha * alpha + ss), alpha); tau = (beta - alpha) / beta; }
+        const double scale = (tau == 0.0) ? 0.0 : 1.0 / (alpha - beta);
+        for (int i = lane; i < p; i += 32) vb[0][i] = (i < 1) ? 0.0 : (i == 1 ? 1.0 : A[i] * scale);
+        if (lane == 0) { s_tau[0] = tau; s_beta[0] = beta; }
+        if (blockIdx.x == 0 && lane == 0) a.d[0] = A[0];
+    }
+    __syncthreads();
+    if (owner && g >= 1) {
+        const double *v = vb[0];
+        double ss = 0.0;
+#pragma unroll
+        for (int u = 0; u < CH; u++) { const int i = lane + 32 * u; if (i >= 1 && i < p) ss = fma(col[u], v[i], ss); }
+        ss = warp_sum(ss);
+        if (lane == 0) a.P[g] = s_tau[0] * ss;
+    }
+    grid.sync();
+    for (int j = 0; j + 2 < p; j++) {
+        const int cur = j & 1, nxt = cur ^ 1;
+        const int r0 = j + 1;
+        const double *v = vb[cur];
+        double *vn = vb[nxt];
+        const bool more = (j + 3 < p);
+        // three block barriers per column; every reduction is warp shuffles + one
+        // shared-memory partial per warp (summed in the same order by every thread)
+        const double tau = s_tau[cur], beta = s_beta[cur];
+        const double *cj = A + (long)r0 * p;
+        double part = 0.0;
+        for (int i = r0 + threadIdx.x; i < p; i += blockDim.x) {
+            const double t = a.P[i];
+            w[i] = t;
+            vn[i] = cj[i];
+            part = fma(t, v[i], part);
+        }
+        part = warp_sum(part);
+        if (lane == 0) red1[wid] = part;
+        __syncthreads();
+        double kk = 0.0;
+        for (int q = 0; q < nwb; q++) kk += red1[q];
+        kk *= 0.5 * tau;
+        const double wr0 = a.P[r0] - kk * v[r0];
+        part = 0.0;
+        for (int i = r0 + threadIdx.x; i < p; i += blockDim.x) {
+            const double wi = fma(-kk, v[i], w[i]);
+            w[i] = wi;
+            const double c = vn[i] - v[i] * wr0 - wi;                  // column j+1 after step j (v[r0] = 1)
+            vn[i] = c;
+            if (i >= r0 + 2) part = fma(c, c, part);
+        }
+        part = warp_sum(part);
+        if (lane == 0) red2[wid] = part;
+        __syncthreads();
+        {
+            double ss = 0.0;
+            for (int q = 0; q < nwb; q++) ss += red2[q];
+            const double alpha = vn[r0 + 1];
+            double taun = 0.0, betan = alpha;
+            if (more && ss != 0.0) { betan = -copysign(sqrt(alpha * alpha + ss), alpha); taun = (betan - alpha) / betan; }
+            const double dj1 = vn[r0];
+            const double scale = (taun == 0.0) ? 0.0 : 1.0 / (alpha - betan);
+            __syncthreads();                                             // alpha, dj1 read before vn is rescaled
+            for (int i = r0 + threadIdx.x; i < p; i += blockDim.x)
+                vn[i] = (i == r0) ? 0.0 : (i == r0 + 1 ? 1.0 : vn[i] * scale);
+            if (threadIdx.x == 0) { s_tau[nxt] = taun; s_beta[nxt] = betan; }
+            if (blockIdx.x == 0) {
+                for (int i = r0 + threadIdx.x; i < p; i += blockDim.x) a.R[(long)j * p + i] = v[i];
+                if (threadIdx.x == 0) {
+                    a.e[j] = beta; a.tau[j] = tau; a.d[j + 1] = dj1;
+                    if (!more) { a.e[j + 1] = alpha; a.tau[j + 1] = 0.0; }
+                }
+            }
+        }
+        __syncthreads();
+        if (owner && g >= r0 + 1) {
+            const double vg = v[g], wg = w[g];
+            double ss = 0.0;
+#pragma unroll
+            for (int u = 0; u < CH; u++) {
+                const int i = lane + 32 * u;
+                if (i >= r0 + 1 && i < p) {
+                    const double x = col[u] - v[i] * wg - w[i] * vg;
+                    col[u] = x;
+                    if (more) ss = fma(x, vn[i], ss);
+                }
+            }
+            if (more) {
+                ss = warp_sum(ss);
+                if (lane == 0) a.P[g] = s_tau[nxt] * ss;
+            }
+            if (g == r0 + 1) {
+#pragma unroll
+                for (int u = 0; u < CH; u++) {
+                    const int i = lane + 32 * u;
+                    if (i >= r0 + 1 && i < p) A[(long)g * p + i] = col[u];
+                }
+            }
+            if (g == p - 1 && !more) {
+#pragma unroll
+                for (int u = 0; u < CH; u++) if (lane + 32 * u == p - 1) a.d[p - 1] = col[u];
+            }
+        }
+        grid.sync();
+    }
+}
+
 // (previous two-barrier version kept for reference in the git history)
 __global__ void __launch_bounds__(256)
 tridiag_kernel_2sync(TridArgs a)
@@ -779,10 +916,18 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
                 cudaFuncSetAttribute(tridiag_reg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
                 cudaFuncSetAttribute(tridiag_reg_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
                 cudaFuncSetAttribute(tridiag_reg_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                cudaFuncSetAttribute(tridiag_w_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                cudaFuncSetAttribute(tridiag_w_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                cudaFuncSetAttribute(tridiag_w_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
                 attr2 = true;
             }
-            void *fn = (p <= 256) ? (void *)tridiag_reg_kernel<8>
-                     : (p <= 512) ? (void *)tridiag_reg_kernel<16> : (void *)tridiag_reg_kernel<32>;
+            void *fn;
+            if (env_flag("LYAP_TRIDIAG_REG"))
+                fn = (p <= 256) ? (void *)tridiag_reg_kernel<8>
+                   : (p <= 512) ? (void *)tridiag_reg_kernel<16> : (void *)tridiag_reg_kernel<32>;
+            else
+                fn = (p <= 256) ? (void *)tridiag_w_kernel<8>
+                   : (p <= 512) ? (void *)tridiag_w_kernel<16> : (void *)tridiag_w_kernel<32>;
             LYAP_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(need), dim3(256), args, smem, s));
         } else {
             int grid = std::min(max_blocks, std::max(1, p / 4));
