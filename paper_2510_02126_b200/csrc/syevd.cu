@@ -626,27 +626,49 @@ dc_merge_prep_kernel(int p, const MergeInfo *__restrict__ mi, const double *__re
 
 // M2: gather Q block columns into sorted order (Qg[:, lo+k] = Q[:, lo+perm[k]], rows lo..hi),
 // apply the deflation rotations in order (each thread one row), and compact the
-// non-deflated columns into Qk[:, lo+k] = Qg[:, lo+Kpos[k]].
-__global__ void dc_gather_rotate_kernel(int p, const MergeInfo *__restrict__ mi, const double *__restrict__ Q,
-                                        const int *__restrict__ perm, const double *__restrict__ rot,
-                                        const int *__restrict__ counts, const int *__restrict__ Kpos,
-                                        double *__restrict__ Qg, double *__restrict__ Qk)
+// non-deflated columns into Qk[:, lo+k] = Qg[:, lo+Kpos[k]].  Gather and compaction run
+// over (row, column) in parallel (grid.y strides columns, grid.z = subproblem); only the
+// rotations, which must be applied in order, are one thread per row.
+__global__ void dc_gather_kernel(int p, const MergeInfo *__restrict__ mi, const double *__restrict__ Q,
+                                 const int *__restrict__ perm, double *__restrict__ Qg)
+{
+    const MergeInfo m = mi[blockIdx.z];
+    const int lo = m.lo, n = m.hi - m.lo;
+    for (int k = blockIdx.y; k < n; k += gridDim.y) {
+        const double *src = Q + (long)(lo + perm[lo + k]) * p + lo;
+        double *dst = Qg + (long)(lo + k) * p + lo;
+        for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) dst[r] = src[r];
+    }
+}
+__global__ void dc_rotate_kernel(int p, const MergeInfo *__restrict__ mi, const double *__restrict__ rot,
+                                 const int *__restrict__ counts, double *__restrict__ Qg)
 {
     const MergeInfo m = mi[blockIdx.y];
     const int lo = m.lo, n = m.hi - m.lo;
-    const int kk = counts[2 * blockIdx.y], nr = counts[2 * blockIdx.y + 1];
+    const int nr = counts[2 * blockIdx.y + 1];
+    if (nr == 0) return;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-        for (int k = 0; k < n; k++) Qg[(long)(lo + k) * p + lo + r] = Q[(long)(lo + perm[lo + k]) * p + lo + r];
         for (int t = 0; t < nr; t++) {
             const double *R = rot + 4 * (lo + t);
-            int a = (int)R[0], b = (int)R[1];
-            double c = R[2], s = R[3];
+            const int a = (int)R[0], b = (int)R[1];
+            const double c = R[2], s = R[3];
             double *xa = Qg + (long)(lo + a) * p + lo + r, *xb = Qg + (long)(lo + b) * p + lo + r;
-            double x = *xa, y = *xb;
+            const double x = *xa, y = *xb;
             *xa = c * x + s * y;
             *xb = c * y - s * x;
         }
-        for (int k = 0; k < kk; k++) Qk[(long)(lo + k) * p + lo + r] = Qg[(long)(lo + Kpos[lo + k]) * p + lo + r];
+    }
+}
+__global__ void dc_compact_kernel(int p, const MergeInfo *__restrict__ mi, const int *__restrict__ counts,
+                                  const int *__restrict__ Kpos, const double *__restrict__ Qg, double *__restrict__ Qk)
+{
+    const MergeInfo m = mi[blockIdx.z];
+    const int lo = m.lo, n = m.hi - m.lo;
+    const int kk = counts[2 * blockIdx.z];
+    for (int k = blockIdx.y; k < kk; k += gridDim.y) {
+        const double *src = Qg + (long)(lo + Kpos[lo + k]) * p + lo;
+        double *dst = Qk + (long)(lo + k) * p + lo;
+        for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) dst[r] = src[r];
     }
 }
 
@@ -683,15 +705,28 @@ __global__ void dc_secular_kernel(const MergeInfo *__restrict__ mi, const double
         double a, b;                          // tau interval
         if (o == j) { a = 0.0; b = (j + 1 < kk) ? 0.5 * (du - dl) : du - dl; }
         else { a = -(0.5 * (du - dl)); b = 0.0; }
-        for (int it = 0; it < 400; it++) {
-            double c = 0.5 * (a + b);
-            if (c == a || c == b) break;
-            double f = 0.0;
-            for (int i = lane; i < kk; i += 32) f += z[i] * z[i] / ((D[i] - Do) - c);
+        // safeguarded Newton on f(tau) = 1 + rho sum z_i^2 / (delta_i - tau), f increasing on
+        // (a, b): the bracket shrinks with the sign of f, Newton steps leaving it are
+        // replaced by bisection; stop at a relative step of 2 ulp or a collapsed bracket
+        double tau = 0.5 * (a + b);
+        for (int it = 0; it < 200; it++) {
+            double f = 0.0, df = 0.0;
+            for (int i = lane; i < kk; i += 32) {
+                const double t = z[i] / ((D[i] - Do) - tau);
+                f = fma(t, z[i], f);
+                df = fma(t, t, df);
+            }
             f = 1.0 + rho * warp_sum(f);
-            if (f > 0.0) b = c; else a = c;
+            df = rho * warp_sum(df);
+            if (f == 0.0) break;
+            if (f > 0.0) b = tau; else a = tau;
+            double tn = tau - f / df;
+            if (!(tn > a && tn < b)) tn = 0.5 * (a + b);
+            const bool done = (tn == a || tn == b || fabs(tn - tau) <= 4.4e-16 * fabs(tn));
+            tau = tn;
+            if (done) break;
         }
-        if (lane == 0) { taus[lo + j] = 0.5 * (a + b); orig[lo + j] = o; }
+        if (lane == 0) { taus[lo + j] = tau; orig[lo + j] = o; }
     }
 }
 
@@ -969,8 +1004,15 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
         int maxn = 0;
         for (auto &x : hm) maxn = std::max(maxn, x.hi - x.lo);
         dim3 g1(ceil_div(maxn, 128), nm);
-        dc_gather_rotate_kernel<<<g1, 128, 0, s>>>(p, mi, W.Q, perm, W.rot, counts, Kpos, W.Qg, W.Qk);
-        LYAP_TRY(launched());
+        {
+            const dim3 gc(ceil_div(maxn, 128), std::min(maxn, std::max(1, 2048 / nm)), nm);
+            dc_gather_kernel<<<gc, 128, 0, s>>>(p, mi, W.Q, perm, W.Qg);
+            LYAP_TRY(launched());
+            dc_rotate_kernel<<<g1, 128, 0, s>>>(p, mi, W.rot, counts, W.Qg);
+            LYAP_TRY(launched());
+            dc_compact_kernel<<<gc, 128, 0, s>>>(p, mi, counts, Kpos, W.Qg, W.Qk);
+            LYAP_TRY(launched());
+        }
         dc_secular_kernel<<<dim3(ceil_div((long)maxn * 32, 256), nm), 256, 0, s>>>(mi, DK, zK, counts, rho, taus, orig);
         LYAP_TRY(launched());
         dc_vectors_kernel<<<g1, 128, 0, s>>>(p, mi, DK, zK, counts, rho, taus, orig, zhat, W.U);
