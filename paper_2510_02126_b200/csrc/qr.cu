@@ -40,6 +40,17 @@ __device__ __forceinline__ double reduce_scatter32(double (&d)[QB], int lane)
     return d[0];
 }
 
+__device__ __forceinline__ double sel_col32(const double (&r)[QB], int j) {
+    double v = r[0];
+#pragma unroll
+    for (int c = 1; c < QB; c++) v = (c == j) ? r[c] : v;
+    return v;
+}
+__device__ __forceinline__ void set_col32(double (&r)[QB], int j, double x) {
+#pragma unroll
+    for (int c = 0; c < QB; c++) r[c] = (c == j) ? x : r[c];
+}
+
 // Factor panel columns [j0, j0+jb) of W (m x n, ld m), rows j0..m-1.
 // Writes V (m x k, ld m; zero above the diagonal), tau, and T_panel (QB x QB).
 // Row-distributed: per reflector, every thread forms the dot products of v with all
@@ -338,6 +349,189 @@ qr_panel_cluster_kernel(int m, int j0, int jb, int RB, double *__restrict__ W, d
     cl.sync();                                     // no CTA leaves while its shared memory may be read
 }
 
+// ---------------------------------------------------------------------------------
+// Register panel: the same reflectors with every panel row held in registers by one
+// thread (256 threads per CTA, cluster of NC = ceil(R/256) CTAs, R <= 4096).  One
+// cluster exchange per reflector in the common case: the partial dot products of v
+// with all 32 panel columns are pushed into every CTA's inbox together with the
+// pre-update sums that give the next column's trailing norm by downdating,
+//     s' = S_xx - 2 f S_vx + f^2 S_vv   (f = tau d_{j+1}),
+// which is used only when s' >= S_xx / 2 (no cancellation: error a few ulp);
+// otherwise a second exchange computes s' directly.
+constexpr int QRT = 256, QNV = QB + 5;     // 32 dots + S_xx, S_vx, S_vv, x_{j+1}, v_{j+1}
+
+template <int NV>
+__device__ __forceinline__ void qr_cta_reduce_push(double (&vals)[NV], int lane, int wid, int q, int NC,
+                                                   double (*part)[NV + 1], double (*inbox)[NV + 1],
+                                                   cooperative_groups::cluster_group &cl)
+{
+    // lanes: reduce-scatter of the first 32 values, plain sums of the rest (lane 0)
+    double d[QB];
+#pragma unroll
+    for (int c = 0; c < QB; c++) d[c] = vals[c];
+    const double col = reduce_scatter32(d, lane);
+    if constexpr (NV > QB) {
+#pragma unroll
+        for (int e = QB; e < NV; e++) vals[e] = warp_sum(vals[e]);
+    }
+    part[wid][lane] = col;
+    if constexpr (NV > QB) {
+        if (lane == 0)
+#pragma unroll
+            for (int e = QB; e < NV; e++) part[wid][e] = vals[e];
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < NV) {
+        double acc = 0.0;
+        for (int w = 0; w < QRT / 32; w++) acc += part[w][t];
+        for (int r = 0; r < NC; r++) cl.map_shared_rank(&inbox[0][0], r)[q * (NV + 1) + t] = acc;
+    }
+    cl.sync();
+}
+
+__global__ void __launch_bounds__(QRT)
+qr_panel_reg_kernel(int m, int j0, int jb, double *__restrict__ W, double *__restrict__ V,
+                    double *__restrict__ tau, double *__restrict__ diag, double *__restrict__ Tp)
+{
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int q = (int)cl.block_rank(), NC = (int)cl.num_blocks();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int R = m - j0;
+    const int gi = q * QRT + tid;                          // this thread's panel row
+    const bool has = gi < R;
+    __shared__ double part[QRT / 32][QNV + 1];
+    __shared__ double inbox[2][16][QNV + 1];
+    __shared__ double tot[QNV];
+    __shared__ double G[QB][QB + 1];
+    __shared__ double tl[QB];
+    double row[QB];
+#pragma unroll
+    for (int c = 0; c < QB; c++) row[c] = (has && c < jb) ? W[(long)(j0 + c) * m + j0 + gi] : 0.0;
+    // column 0: trailing norm and pivot entry (second-exchange path)
+    double s, x0;
+    {
+        double vals[2] = {(has && gi >= 1) ? row[0] * row[0] : 0.0, (has && gi == 0) ? row[0] : 0.0};
+#pragma unroll
+        for (int e = 0; e < 2; e++) vals[e] = warp_sum(vals[e]);
+        if (lane == 0) { part[wid][0] = vals[0]; part[wid][1] = vals[1]; }
+        __syncthreads();
+        if (tid < 2) {
+            double acc = 0.0;
+            for (int w = 0; w < QRT / 32; w++) acc += part[w][tid];
+            for (int r = 0; r < NC; r++) cl.map_shared_rank(&inbox[1][0][0], r)[q * (QNV + 1) + tid] = acc;
+        }
+        cl.sync();
+        s = 0.0; x0 = 0.0;
+        for (int r = 0; r < NC; r++) { s += inbox[1][r][0]; x0 += inbox[1][r][1]; }
+        __syncthreads();
+    }
+    for (int jj = 0; jj < jb; jj++) {
+        const int buf = jj & 1;
+        double tj = 0.0, v0 = 0.0, alpha = 0.0;
+        const double nrm2 = s + x0 * x0;
+        if (nrm2 != 0.0) {
+            alpha = (x0 >= 0.0) ? -sqrt(nrm2) : sqrt(nrm2);
+            v0 = x0 - alpha;
+            tj = 2.0 / (v0 * v0 + s);
+        }
+        const double vi = (!has || gi < jj || tj == 0.0) ? 0.0 : (gi == jj ? v0 : sel_col32(row, jj));
+        const double xn = sel_col32(row, jj + 1 < QB ? jj + 1 : QB - 1);
+        const bool below = has && gi > jj + 1 && jj + 1 < jb;
+        double vals[QNV];
+#pragma unroll
+        for (int c = 0; c < QB; c++) vals[c] = vi * row[c];
+        vals[QB + 0] = below ? xn * xn : 0.0;
+        vals[QB + 1] = below ? vi * xn : 0.0;
+        vals[QB + 2] = below ? vi * vi : 0.0;
+        vals[QB + 3] = (has && gi == jj + 1) ? xn : 0.0;
+        vals[QB + 4] = (has && gi == jj + 1) ? vi : 0.0;
+        qr_cta_reduce_push<QNV>(vals, lane, wid, q, NC, part, inbox[buf], cl);
+        if (tid < QNV) {
+            double acc = 0.0;
+            for (int r = 0; r < NC; r++) acc += inbox[buf][r][tid];
+            tot[tid] = acc;
+        }
+        __syncthreads();
+        if (q == 0 && tid < jj) G[tid][jj] = tot[tid];
+        if (tid == 0) {
+            tl[jj] = tj;
+            if (q == 0) { tau[j0 + jj] = tj; diag[j0 + jj] = (tj == 0.0) ? 0.0 : alpha; }
+        }
+        // apply H_jj to columns jj+1..; column jj keeps v (v0 on the diagonal row)
+        if (has && gi >= jj) {
+            const double f = tj * vi;
+#pragma unroll
+            for (int c = 0; c < QB; c++) {
+                const double y = fma(-f, tot[c], row[c]);
+                row[c] = (c > jj && c < jb) ? y : row[c];
+            }
+            if (gi == jj && tj != 0.0) set_col32(row, jj, v0);
+        }
+        if (jj + 1 < jb) {
+            // next column: downdated trailing norm, or a second exchange on cancellation
+            const double f = tj * tot[jj + 1];
+            const double sxx = tot[QB], svx = tot[QB + 1], svv = tot[QB + 2];
+            const double sd = sxx - 2.0 * f * svx + f * f * svv;
+            x0 = tot[QB + 3] - f * tot[QB + 4];
+            if (sd >= 0.5 * sxx) {
+                s = sd;
+            } else {
+                const double xv = sel_col32(row, jj + 1);
+                double v2[2] = {below ? xv * xv : 0.0, 0.0};
+                v2[0] = warp_sum(v2[0]);
+                __syncthreads();                                // tot / part reads above are done
+                if (lane == 0) part[wid][0] = v2[0];
+                __syncthreads();
+                if (tid == 0) {
+                    double acc = 0.0;
+                    for (int w = 0; w < QRT / 32; w++) acc += part[w][0];
+                    for (int r = 0; r < NC; r++) cl.map_shared_rank(&inbox[buf ^ 1][0][0], r)[q * (QNV + 1) + QNV] = acc;
+                }
+                cl.sync();
+                s = 0.0;
+                for (int r = 0; r < NC; r++) s += inbox[buf ^ 1][r][QNV];
+            }
+        }
+        __syncthreads();
+    }
+    // V (this CTA's rows), the R part above the diagonal, T on CTA 0
+    if (has) {
+#pragma unroll
+        for (int c = 0; c < QB; c++) {
+            if (c < jb) {
+                const int j = j0 + c;
+                V[(long)j * m + j0 + gi] = (tl[c] != 0.0 && gi >= c) ? row[c] : 0.0;
+                if (gi != c) W[(long)j * m + j0 + gi] = (gi < c) ? row[c] : 0.0;
+            }
+        }
+    }
+    if (q == 0)
+        for (int c = 0; c < jb; c++)
+            for (int i = tid; i < j0; i += QRT) V[(long)(j0 + c) * m + i] = 0.0;
+    if (q == 0 && tid < 32) {
+        const int a = tid;
+        double Ta[QB];
+#pragma unroll
+        for (int c = 0; c < QB; c++) Ta[c] = 0.0;
+#pragma unroll
+        for (int c = 0; c < QB; c++) {
+            if (c < jb) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int l = 0; l < c; l++)
+                    if (l >= a) sacc = fma(Ta[l], G[l][c], sacc);
+                const double tc = tl[c];
+                Ta[c] = (a < c) ? -tc * sacc : ((a == c) ? tc : 0.0);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < QB; c++) Tp[a + c * QB] = Ta[c];
+    }
+    cl.sync();
+}
+
 __global__ void set_identity_kernel(int m, int k, double *Q) {
     long tot = (long)m * k;
     for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < tot; idx += (long)gridDim.x * blockDim.x) {
@@ -428,7 +622,28 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
     for (size_t pi = 0; pi + 1 < starts.size(); pi++) {
         const int j0 = starts[pi], jb = starts[pi + 1] - j0;
         double *Tp = w.T + pi * QB * QB;
-        if (use_cluster) {
+        if (m - j0 <= 16 * QRT && !env_flag("LYAP_QR_SMEM")) {
+            const int nc = ceil_div(m - j0, QRT);
+            KTimer kp(KC_QR_PANEL, s, 4.0 * (m - j0) * jb * jb, 16.0 * (m - j0) * jb);
+            static bool attr_r = false;
+            if (!attr_r) {
+                LYAP_CUDA_TRY(cudaFuncSetAttribute(qr_panel_reg_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                attr_r = true;
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(nc, 1, 1);
+            cfg.blockDim = dim3(QRT, 1, 1);
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = nc;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            LYAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel, m, j0, jb, Wm, w.V, w.tau, diag, Tp));
+            LYAP_TRY(launched());
+        } else if (use_cluster) {
             const int RB = ceil_div(m - j0, QC);
             KTimer kp(KC_QR_PANEL, s, 4.0 * (m - j0) * jb * jb, 16.0 * (m - j0) * jb);
             qr_panel_cluster_kernel<<<QC, QCT, sizeof(double) * RB * QB, s>>>(m, j0, jb, RB, Wm, w.V, w.tau, diag,
