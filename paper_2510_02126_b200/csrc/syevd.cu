@@ -850,6 +850,60 @@ __global__ void wy_T_kernel(int jb, const double *__restrict__ G, const double *
     for (int c = 0; c < 32; c++) Tp[a + c * 32] = Ta[c];
 }
 
+// All compact-WY triangular factors of the back-transformation at once: CTA = panel of
+// 32 reflectors; Gram G = V^T V over the panel's nonzero rows (staged 64 rows at a time),
+// then T by the wy_T_kernel recurrence (lane a keeps row a of T).
+__global__ void __launch_bounds__(256)
+wy_gramT_batched_kernel(int p, int nref, const double *__restrict__ R, const double *__restrict__ tau,
+                        double *__restrict__ Tall)
+{
+    const int panel = blockIdx.x, j0 = panel * 32, jb = min(32, nref - j0);
+    const double *Vp = R + (long)j0 * p;
+    __shared__ double Vs[64][33];
+    __shared__ double Gs[32][33];
+    const int tid = threadIdx.x;
+    const int ga = tid >> 3, c0 = (tid & 7) * 4;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int r0 = j0 + 1; r0 < p; r0 += 64) {
+        for (int e = tid; e < 64 * 32; e += 256) {
+            const int i = e & 63, cc = e >> 6;
+            Vs[i][cc] = (r0 + i < p && cc < jb) ? Vp[(long)cc * p + r0 + i] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int i = 0; i < 64; i++) {
+            const double va = Vs[i][ga];
+#pragma unroll
+            for (int t = 0; t < 4; t++) acc[t] = fma(va, Vs[i][c0 + t], acc[t]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int t = 0; t < 4; t++) Gs[c0 + t][ga] = acc[t];           // Gs[c][l] = G(l, c)
+    __syncthreads();
+    if (tid < 32) {
+        const int a = tid;
+        const double *tp = tau + j0;
+        double Ta[32];
+#pragma unroll
+        for (int c = 0; c < 32; c++) Ta[c] = 0.0;
+#pragma unroll
+        for (int c = 0; c < 32; c++) {
+            if (c < jb) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int l = 0; l < c; l++)
+                    if (l >= a) sacc = fma(Ta[l], Gs[c][l], sacc);
+                const double tc = tp[c];
+                Ta[c] = (a < c) ? -tc * sacc : ((a == c) ? tc : 0.0);
+            }
+        }
+        double *Tp = Tall + (long)panel * 1024;
+#pragma unroll
+        for (int c = 0; c < 32; c++) Tp[a + c * 32] = Ta[c];
+    }
+}
+
 // eigenvalues descending + sign normalisation (largest |component| positive, lowest index)
 __global__ void eigfinal_kernel(int p, const double *__restrict__ lam, const double *__restrict__ X,
                                 double *__restrict__ w, double *__restrict__ V)
@@ -1038,15 +1092,16 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
     if (prof) cudaEventRecord(pev[2], s);
     // 3. back-transformation X = Q_H Q_T: panels of 32 reflectors, last panel first
     const int nref = std::max(p - 2, 0);
+    if (nref > 0) {
+        wy_gramT_batched_kernel<<<ceil_div(nref, 32), 256, 0, s>>>(p, nref, W.R, tau, Tp);
+        LYAP_TRY(launched());
+    }
     for (int j0 = ((nref - 1) / 32) * 32; nref > 0 && j0 >= 0; j0 -= 32) {
         const int jb = std::min(32, nref - j0);
         // V = reflectors j0..j0+jb-1 as stored (zero above the unit entry), p x jb, ld p
         const double *Vp = W.R + (size_t)j0 * p;
-        LYAP_TRY(dgemm_cm(s, true, false, jb, jb, p, 1.0, Vp, p, Vp, p, 0.0, W.Qk, 32));
-        wy_T_kernel<<<1, 32, 0, s>>>(jb, W.Qk, tau + j0, Tp);
-        LYAP_TRY(launched());
         // X <- (I - V T V^T) X over rows j0+1..p-1 (reflector j0+a is zero above row j0+a+1)
-        LYAP_TRY(wy_apply(s, p, p, jb, j0 + 1, Vp, p, Tp, 0, W.Q, p));
+        LYAP_TRY(wy_apply(s, p, p, jb, j0 + 1, Vp, p, Tp + (size_t)(j0 / 32) * 1024, 0, W.Q, p));
     }
     eigfinal_kernel<<<std::min(ceil_div((long)p * 32, 256), 1024), 256, 0, s>>>(p, lam, W.Q, w_out, V_out);
     LYAP_TRY(launched());
