@@ -134,35 +134,47 @@ newton_update_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ G, c
 
 // ------------------------------------------------------------ Z side
 // Zt (n x m, T) = round(2^{-e} L) with e = exponent of max|L| (computed here, one CTA).
-template <typename T>
-__global__ void __launch_bounds__(1024)
-load_factor_kernel(long len, const double *__restrict__ L, T *__restrict__ Zt, double *__restrict__ scal, int slot)
+// grid-wide max|x| as the bit pattern of a non-negative double (integer order = value
+// order), accumulated with atomicMax into a zeroed slot
+__global__ void absmax_bits_kernel(long len, const double *__restrict__ x, unsigned long long *__restrict__ out)
 {
     __shared__ double red[32];
     double mx = 0.0;
-    for (long i = threadIdx.x; i < len; i += blockDim.x) mx = fmax(mx, fabs(L[i]));
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < len; i += (long)gridDim.x * blockDim.x)
+        mx = fmax(mx, fabs(x[i]));
     mx = block_max(mx, red);
-    int e = 0;
-    if (mx > 0.0 && isfinite(mx)) frexp(mx, &e);
-    if (threadIdx.x == 0) scal[slot] = (double)e;
-    for (long i = threadIdx.x; i < len; i += blockDim.x) Zt[i] = from_d<T>(ldexp(L[i], -e));
+    if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(mx));
 }
 
-// Y (m x m fp64) = round_us(2^{-e} S), e = exponent of max|S|; one CTA.
+__device__ __forceinline__ int exp_of_max(const double *scal) {
+    const double mx = __longlong_as_double((long long)reinterpret_cast<const unsigned long long *>(scal)[SC_MAXB]);
+    int e = 0;
+    if (mx > 0.0 && isfinite(mx)) frexp(mx, &e);
+    return e;
+}
+
+// Zt = 2^{-e} L rounded to T, e = exponent of max|L| (grid-wide, after absmax_bits_kernel)
+template <typename T>
+__global__ void load_factor_kernel(long len, const double *__restrict__ L, T *__restrict__ Zt, double *__restrict__ scal,
+                                   int slot)
+{
+    const int e = exp_of_max(scal);
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < len; i += (long)gridDim.x * blockDim.x)
+        Zt[i] = from_d<T>(ldexp(L[i], -e));
+    if (blockIdx.x == 0 && threadIdx.x == 0) scal[slot] = (double)e;
+}
+
+// Y (m x m fp64) = round_us(2^{-e} S), e = exponent of max|S| (grid-wide)
 __global__ void load_inner_kernel(int m, const double *__restrict__ S, double *__restrict__ Y, int ldy,
                                   int prec, double *__restrict__ scal, int slot)
 {
-    __shared__ double red[32];
-    double mx = 0.0;
-    for (int i = threadIdx.x; i < m * m; i += blockDim.x) mx = fmax(mx, fabs(S[i]));
-    mx = block_max(mx, red);
-    int e = 0;
-    if (mx > 0.0 && isfinite(mx)) frexp(mx, &e);
-    if (threadIdx.x == 0) scal[slot] = (double)e;
-    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-        int i = idx % m, j = idx / m;
+    const int e = exp_of_max(scal);
+    const long tot = (long)m * m;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < tot; idx += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx % m), j = (int)(idx / m);
         Y[i + (long)j * ldy] = round_to(ldexp(S[idx], -e), prec);
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) scal[slot] = (double)e;
 }
 
 // Ynew (2c x 2c, ld ldn) = blkdiag(round(a Y), round(b Y)) with a = mu/2, b = 1/(2 mu).
@@ -410,15 +422,23 @@ int nk_update(cudaStream_t s, int prec, int n, const void *Ak, const void *G, co
 }
 
 template <typename T> static void k_loadf(cudaStream_t s, long len, const double *L, void *Zt, double *scal, int slot)
-{ load_factor_kernel<T><<<1, 1024, 0, s>>>(len, L, (T *)Zt, scal, slot); }
+{ load_factor_kernel<T><<<grid_for(len), 256, 0, s>>>(len, L, (T *)Zt, scal, slot); }
+static int absmax_bits(cudaStream_t s, long len, const double *x, double *scal)
+{
+    LYAP_CUDA_TRY(cudaMemsetAsync(scal + SC_MAXB, 0, sizeof(double), s));
+    absmax_bits_kernel<<<grid_for(len), 256, 0, s>>>(len, x, reinterpret_cast<unsigned long long *>(scal) + SC_MAXB);
+    return launched();
+}
 int nk_load_factor(cudaStream_t s, int prec, long len, const double *L, void *Zt, double *scal, int slot)
 {
+    LYAP_TRY(absmax_bits(s, len, L, scal));
     DISPATCH_T(prec, k_loadf, s, len, L, Zt, scal, slot);
     return launched();
 }
 int nk_load_inner(cudaStream_t s, int prec, int m, const double *S, double *Y, int ldy, double *scal, int slot)
 {
-    load_inner_kernel<<<1, 256, 0, s>>>(m, S, Y, ldy, prec, scal, slot);
+    LYAP_TRY(absmax_bits(s, (long)m * m, S, scal));
+    load_inner_kernel<<<grid_for((long)m * m), 256, 0, s>>>(m, S, Y, ldy, prec, scal, slot);
     return launched();
 }
 int nk_y_blkdiag(cudaStream_t s, int c, const double *Y, int ldy, double *Yn, int ldn, double a, double b, int prec)

@@ -16,6 +16,7 @@ enum {
     SC_EL2 = 10,     // second right-hand side (Cholesky minus equation)
     SC_TR = 11,      // trace results (norms of implied products)
     SC_TR2 = 12,
+    SC_MAXB = 13,    // scratch: bit pattern of a grid-wide max|x| (atomicMax on non-negative doubles)
     SC_COUNT = 16
 };
 
