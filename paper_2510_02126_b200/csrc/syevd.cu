@@ -277,52 +277,70 @@ tridiag_w_kernel(TridArgs a)
         if (lane == 0) a.P[g] = s_tau[0] * ss;
     }
     grid.sync();
+#ifdef LYAP_PANEL_PROF
+    long long pt[6] = {0, 0, 0, 0, 0, 0}, tl = clock64();
+#define TPROF(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) { long long t_ = clock64(); pt[i] += t_ - tl; tl = t_; } } while (0)
+#else
+#define TPROF(i) do { } while (0)
+#endif
     for (int j = 0; j + 2 < p; j++) {
         const int cur = j & 1, nxt = cur ^ 1;
         const int r0 = j + 1;
         const double *v = vb[cur];
         double *vn = vb[nxt];
         const bool more = (j + 3 < p);
-        // three block barriers per column; every reduction is warp shuffles + one
-        // shared-memory partial per warp (summed in the same order by every thread)
+        // One block reduction per column: with y = x - P (x = column j+1 as published,
+        // P = tau A v), the updated column is c = y + t v, t = 2k - P[r0], so
+        //   k = (tau/2) P.v   and   ||c[r0+2:]||^2 = S_yy + 2 t S_yv + t^2 S_vv
+        // come from four partial sums of one pass; on cancellation (result < 1/4 of the
+        // terms) the norm is recomputed exactly with a second reduction.
         const double tau = s_tau[cur], beta = s_beta[cur];
         const double *cj = A + (long)r0 * p;
-        double part = 0.0;
+        double pv = 0.0, yy = 0.0, yv = 0.0, vv = 0.0;
         for (int i = r0 + threadIdx.x; i < p; i += blockDim.x) {
-            const double t = a.P[i];
-            w[i] = t;
-            vn[i] = cj[i];
-            part = fma(t, v[i], part);
+            const double Pi = a.P[i], vi = v[i], yi = cj[i] - Pi;
+            w[i] = Pi;
+            vn[i] = yi;
+            pv = fma(Pi, vi, pv);
+            if (i >= r0 + 2) { yy = fma(yi, yi, yy); yv = fma(yi, vi, yv); vv = fma(vi, vi, vv); }
         }
-        part = warp_sum(part);
-        if (lane == 0) red1[wid] = part;
+        pv = warp_sum(pv); yy = warp_sum(yy); yv = warp_sum(yv); vv = warp_sum(vv);
+        if (lane == 0) { red1[wid] = pv; red1[8 + wid] = yy; red1[16 + wid] = yv; red2[wid] = vv; }
+        const double P0 = a.P[r0], y0 = cj[r0] - P0;
+        const double P1 = (r0 + 1 < p) ? a.P[r0 + 1] : 0.0, y1 = (r0 + 1 < p) ? cj[r0 + 1] - P1 : 0.0;
+        TPROF(0);
         __syncthreads();
-        double kk = 0.0;
-        for (int q = 0; q < nwb; q++) kk += red1[q];
-        kk *= 0.5 * tau;
-        const double wr0 = a.P[r0] - kk * v[r0];
-        part = 0.0;
-        for (int i = r0 + threadIdx.x; i < p; i += blockDim.x) {
-            const double wi = fma(-kk, v[i], w[i]);
-            w[i] = wi;
-            const double c = vn[i] - v[i] * wr0 - wi;                  // column j+1 after step j (v[r0] = 1)
-            vn[i] = c;
-            if (i >= r0 + 2) part = fma(c, c, part);
+        TPROF(1);
+        double spv = 0.0, syy = 0.0, syv = 0.0, svv = 0.0;
+        for (int q = 0; q < nwb; q++) { spv += red1[q]; syy += red1[8 + q]; syv += red1[16 + q]; svv += red2[q]; }
+        const double kk = 0.5 * tau * spv;
+        const double t = 2.0 * kk - P0;
+        double ss = syy + 2.0 * t * syv + t * t * svv;
+        if (!(ss >= 0.25 * (syy + t * t * svv))) {                 // cancellation: exact norm
+            __syncthreads();                                         // red1/red2 reads done
+            double part = 0.0;
+            for (int i = r0 + 2 + threadIdx.x; i < p; i += blockDim.x) {
+                const double c = fma(t, v[i], vn[i]);
+                part = fma(c, c, part);
+            }
+            part = warp_sum(part);
+            if (lane == 0) red1[wid] = part;
+            __syncthreads();
+            ss = 0.0;
+            for (int q = 0; q < nwb; q++) ss += red1[q];
         }
-        part = warp_sum(part);
-        if (lane == 0) red2[wid] = part;
-        __syncthreads();
+        TPROF(2);
         {
-            double ss = 0.0;
-            for (int q = 0; q < nwb; q++) ss += red2[q];
-            const double alpha = vn[r0 + 1];
+            const double alpha = fma(t, v[r0 + 1 < p ? r0 + 1 : r0], y1);
+            const double dj1 = y0 + t;                               // v[r0] = 1
             double taun = 0.0, betan = alpha;
             if (more && ss != 0.0) { betan = -copysign(sqrt(alpha * alpha + ss), alpha); taun = (betan - alpha) / betan; }
-            const double dj1 = vn[r0];
             const double scale = (taun == 0.0) ? 0.0 : 1.0 / (alpha - betan);
-            __syncthreads();                                             // alpha, dj1 read before vn is rescaled
-            for (int i = r0 + threadIdx.x; i < p; i += blockDim.x)
-                vn[i] = (i == r0) ? 0.0 : (i == r0 + 1 ? 1.0 : vn[i] * scale);
+            for (int i = r0 + threadIdx.x; i < p; i += blockDim.x) {
+                const double vi = v[i];
+                w[i] = fma(-kk, vi, w[i]);
+                vn[i] = (i == r0) ? 0.0 : (i == r0 + 1 ? 1.0 : fma(t, vi, vn[i]) * scale);
+            }
             if (threadIdx.x == 0) { s_tau[nxt] = taun; s_beta[nxt] = betan; }
             if (blockIdx.x == 0) {
                 for (int i = r0 + threadIdx.x; i < p; i += blockDim.x) a.R[(long)j * p + i] = v[i];
@@ -333,6 +351,7 @@ tridiag_w_kernel(TridArgs a)
             }
         }
         __syncthreads();
+        TPROF(3);
         if (owner && g >= r0 + 1) {
             const double vg = v[g], wg = w[g];
             double ss = 0.0;
@@ -361,8 +380,15 @@ tridiag_w_kernel(TridArgs a)
                 for (int u = 0; u < CH; u++) if (lane + 32 * u == p - 1) a.d[p - 1] = col[u];
             }
         }
+        TPROF(4);
         grid.sync();
+        TPROF(5);
     }
+#ifdef LYAP_PANEL_PROF
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("tridiag p=%d grid=%d cycles/col: load+kk %lld bar1 %lld w,c,ss+bar2 %lld refl+bar3 %lld owner %lld gridsync %lld\n",
+               p, gridDim.x, pt[0] / (p - 2), pt[1] / (p - 2), pt[2] / (p - 2), pt[3] / (p - 2), pt[4] / (p - 2), pt[5] / (p - 2));
+#endif
 }
 
 // (previous two-barrier version kept for reference in the git history)
