@@ -203,7 +203,8 @@ int64_t lyap_launch_count(void);
  * every launch of class cls (0 Gauss-Jordan rank-b update GEMM, 1 pivoted
  * panel, 2 A_k^{-1} Z products, 3 Jacobi eigensolver, 4 Householder QR,
  * 5 fp64 A Z, 6 Newton update, 7 fp64 DMMA GEMM, 8 tcgen05 GEMM, 9 Householder
- * panel, 10 tridiagonalisation, 11 compact-WY application; -1 disables) is bracketed by CUDA events on its
+ * panel, 10 tridiagonalisation, 11 compact-WY application, 12 column-pivoted QR;
+ * -1 disables) is bracketed by CUDA events on its
  * launch stream.  lyap_kernel_stats synchronises and returns the summed
  * device milliseconds and the number of timed launches since the last
  * lyap_kernel_timing call. */

@@ -66,7 +66,7 @@ SYMBOLS = ["lyap_ir_default_options", "lyap_ir_create", "lyap_ir_destroy", "lyap
 
 KERNEL_CLASSES = {"gje_update": 0, "gje_panel": 1, "zside_gemm": 2, "eig": 3, "qr": 4,
                   "resid_gemm": 5, "newton_update": 6, "dgemm": 7, "tc_gemm": 8, "qr_panel": 9,
-                  "tridiag": 10, "wy_apply": 11}
+                  "tridiag": 10, "wy_apply": 11, "rrqr": 12}
 
 
 def library_path() -> str:

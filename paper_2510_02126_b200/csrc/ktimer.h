@@ -16,7 +16,8 @@ enum KernelClass {
     KC_TCGEMM = 8,       // tcgen05 16-bit GEMM kernel
     KC_QR_PANEL = 9,     // Householder panel kernel
     KC_TRIDIAG = 10,     // cooperative tridiagonalisation kernel
-    KC_WY = 11           // fused compact-WY block-reflector application
+    KC_WY = 11,          // fused compact-WY block-reflector application
+    KC_RRQR = 12         // column-pivoted QR of RankTruncChol
 };
 
 void ktimer_begin(int cls, cudaStream_t s);

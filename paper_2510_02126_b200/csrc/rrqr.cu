@@ -13,6 +13,7 @@
 #include <cooperative_groups.h>
 #include "common.cuh"
 #include "lyap_internal.h"
+#include "ktimer.h"
 
 namespace cg = cooperative_groups;
 
@@ -132,6 +133,177 @@ rrqr_kernel(RrqrArgs a)
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.rank = rank;
 }
 
+// Second version: one grid barrier per pivot step.  Physical columns never move (the
+// pivot order is kept in perm, and the output needs none: Zout(col, r) = M[col][r]);
+// every warp owns the same columns for the whole factorisation and keeps their
+// trailing norms, downdated after each reflector (||x[j+1:]||^2 = ||x[j:]||^2 - x_j^2)
+// and recomputed exactly when the downdate cancels (LAPACK xLAQP2 rule).  Per step:
+//   grid barrier -> every CTA reduces the per-CTA (sum, argmax) partials identically,
+//   forms the reflector of the pivot column in shared memory -> owners finalise the
+//   previous pivot column, apply H_j to their active columns, downdate, and publish
+//   the next partials.
+struct Rrqr2Args {
+    int n, c, kmax;
+    double tol;
+    double *M;          // c x n col-major
+    double *nrm2;       // n: trailing norm^2 (rows >= current step)
+    double *nrm0;       // n: norm^2 at the last exact recomputation
+    double *bsum;       // 2 x gridDim (double-buffered by step parity)
+    double *bbest;      // 2 x gridDim
+    int *bidx;          // 2 x gridDim
+    int *perm;          // n: pivot order
+    int *active;        // n: 1 while not pivoted
+    double *scal;       // [0] |r_11|
+    int *rank;
+};
+
+__global__ void __launch_bounds__(256)
+rrqr2_kernel(Rrqr2Args a)
+{
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double vsh[];                  // reflector, c entries
+    __shared__ double red[32];
+    __shared__ double s_best[8], s_sum[8];
+    __shared__ int s_idx[8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int gw = blockIdx.x * nwb + wib, nwg = gridDim.x * nwb;
+    const int n = a.n, c = a.c, G = gridDim.x;
+    // initial norms (rows 0..c-1), partials of step 0
+    {
+        double bsum = 0.0, bbest = -1.0; int bidx = n;
+        for (int col = gw; col < n; col += nwg) {
+            const double *x = a.M + (long)col * c;
+            double s = 0.0;
+            for (int i = lane; i < c; i += 32) s = fma(x[i], x[i], s);
+            s = warp_sum(s);
+            if (lane == 0) { a.nrm2[col] = s; a.nrm0[col] = s; a.active[col] = 1; }
+            bsum += s;
+            if (s > bbest || (s == bbest && col < bidx)) { bbest = s; bidx = col; }
+        }
+        if (lane == 0) { s_sum[wib] = bsum; s_best[wib] = bbest; s_idx[wib] = bidx; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0, bv = -1.0; int bi = n;
+            for (int w = 0; w < nwb; w++) {
+                t += s_sum[w];
+                if (s_best[w] > bv || (s_best[w] == bv && s_idx[w] < bi)) { bv = s_best[w]; bi = s_idx[w]; }
+            }
+            a.bsum[blockIdx.x] = t; a.bbest[blockIdx.x] = bv; a.bidx[blockIdx.x] = bi;
+        }
+    }
+    int rank = a.kmax, prev = -1;
+    double r11 = 0.0, prev_alpha = 0.0;
+    for (int j = 0; j < a.kmax; j++) {
+        grid.sync();
+        const int buf = j & 1;
+        const double *bs = a.bsum + buf * G, *bb = a.bbest + buf * G;
+        const int *bx = a.bidx + buf * G;
+        // ---- every CTA: identical reduction of the partials, stop test, pivot
+        double t = 0.0, bv = -1.0; int bi = n;
+        for (int b = lane; b < G; b += 32) {
+            t += bs[b];
+            const double v = bb[b]; const int i2 = bx[b];
+            if (v > bv || (v == bv && i2 < bi)) { bv = v; bi = i2; }
+        }
+        t = warp_sum(t);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; }
+        }
+        const double tr = sqrt(t);
+        const bool stop = (j > 0 && tr <= a.tol * r11) || tr == 0.0 || bi >= n;
+        // owners finalise the previous pivot column (all CTAs have finished reading it)
+        if (prev >= 0 && (prev % nwg) == gw) {
+            double *xp = a.M + (long)prev * c;
+            for (int i = j - 1 + lane; i < c; i += 32) xp[i] = (i == j - 1) ? prev_alpha : 0.0;
+        }
+        if (stop) { rank = j; break; }
+        const int pc = bi;
+        // ---- reflector of column pc, rows j..c-1, in shared memory
+        const double *xp = a.M + (long)pc * c;
+        double part = 0.0;
+        for (int i = j + threadIdx.x; i < c; i += blockDim.x) {
+            const double x = xp[i];
+            vsh[i] = x;
+            if (i > j) part = fma(x, x, part);
+        }
+        part = block_sum(part, red);
+        const double x0 = vsh[j];
+        const double nrm = sqrt(part + x0 * x0);
+        const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+        const double v0 = x0 - alpha;
+        const double vtv = v0 * v0 + part;
+        __syncthreads();
+        if (threadIdx.x == 0) vsh[j] = v0;
+        if (j == 0) r11 = fabs(alpha);
+        if (blockIdx.x == 0 && threadIdx.x == 0) { a.perm[j] = pc; if (j == 0) a.scal[0] = fabs(alpha); }
+        __syncthreads();
+        // ---- owners: apply H_j to active columns, downdate norms, next partials
+        double bsum = 0.0, bbest = -1.0; int bidx = n;
+        for (int col = gw; col < n; col += nwg) {
+            if (col == pc) { if (lane == 0) a.active[col] = 0; continue; }
+            if (!a.active[col]) continue;
+            double *y = a.M + (long)col * c;
+            double d = 0.0;
+            if (vtv != 0.0) {
+                for (int i = j + lane; i < c; i += 32) d = fma(vsh[i], y[i], d);
+                d = warp_sum(d);
+                const double f = 2.0 * d / vtv;
+                for (int i = j + lane; i < c; i += 32) y[i] = fma(-f, vsh[i], y[i]);
+                __syncwarp();
+            }
+            const double yj = y[j];
+            double s2 = a.nrm2[col];
+            const double r = (s2 > 0.0) ? 1.0 - (yj * yj) / s2 : 0.0;
+            const double temp = fmax(r, 0.0);
+            const double temp2 = temp * (s2 / fmax(a.nrm0[col], 1e-300));
+            if (temp2 <= 1.5e-8) {                     // sqrt(eps) rule: recompute exactly
+                double e = 0.0;
+                for (int i = j + 1 + lane; i < c; i += 32) e = fma(y[i], y[i], e);
+                s2 = warp_sum(e);
+                if (lane == 0) a.nrm0[col] = s2;
+            } else {
+                s2 = s2 - yj * yj;
+            }
+            if (lane == 0) a.nrm2[col] = s2;
+            bsum += s2;
+            if (s2 > bbest || (s2 == bbest && col < bidx)) { bbest = s2; bidx = col; }
+        }
+        prev = pc; prev_alpha = alpha;
+        if (lane == 0) { s_sum[wib] = bsum; s_best[wib] = bbest; s_idx[wib] = bidx; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double tt = 0.0, bvv = -1.0; int bii = n;
+            for (int w = 0; w < nwb; w++) {
+                tt += s_sum[w];
+                if (s_best[w] > bvv || (s_best[w] == bvv && s_idx[w] < bii)) { bvv = s_best[w]; bii = s_idx[w]; }
+            }
+            const int nb = buf ^ 1;
+            a.bsum[nb * G + blockIdx.x] = tt; a.bbest[nb * G + blockIdx.x] = bvv; a.bidx[nb * G + blockIdx.x] = bii;
+        }
+    }
+    if (rank == a.kmax && prev >= 0) {                 // finalise the last pivot column
+        grid.sync();
+        if ((prev % nwg) == gw) {
+            double *xp = a.M + (long)prev * c;
+            for (int i = a.kmax - 1 + lane; i < c; i += 32) xp[i] = (i == a.kmax - 1) ? prev_alpha : 0.0;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.rank = rank;
+}
+
+// Zout(col, r) = M[col][r] for r < k, rounded to prec (physical columns = rows of Z)
+__global__ void rrqr2_out_kernel(int n, int c, int k, const double *__restrict__ M, int prec, double *__restrict__ Zout)
+{
+    long tot = (long)n * k;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < tot; idx += (long)gridDim.x * blockDim.x) {
+        const int col = (int)(idx % n), r = (int)(idx / n);
+        Zout[(long)r * n + col] = round_to(M[(long)col * c + r], prec);
+    }
+}
+
 __global__ void transpose_init_kernel(int n, int c, const double *__restrict__ Z, double *__restrict__ M, int *perm)
 {
     long tot = (long)n * c;
@@ -157,8 +329,8 @@ __global__ void rrqr_out_kernel(int n, int c, int k, const double *__restrict__ 
 int RrqrWork::alloc(int nmax_, int cmax_) {
     nmax = nmax_; cmax = cmax_;
     LYAP_CUDA_TRY(cudaMalloc(&M, sizeof(double) * (size_t)nmax * cmax));
-    LYAP_CUDA_TRY(cudaMalloc(&nrm, sizeof(double) * (size_t)(nmax + 3 * 1024 + cmax + 8)));
-    LYAP_CUDA_TRY(cudaMalloc(&ints, sizeof(int) * (size_t)(nmax + 1024 + 8)));
+    LYAP_CUDA_TRY(cudaMalloc(&nrm, sizeof(double) * (size_t)(2 * nmax + 4 * 1024 + cmax + 8)));
+    LYAP_CUDA_TRY(cudaMalloc(&ints, sizeof(int) * (size_t)(2 * nmax + 2048 + 16)));
     scal = nrm + nmax;
     return LYAP_OK;
 }
@@ -168,26 +340,42 @@ int rank_trunc_chol_f64(cudaStream_t s, int n, int c, const double *Z, double to
                         double *Zout, int *k_out, RrqrWork &w)
 {
     if (n > w.nmax || c > w.cmax) return LYAP_ERR_CAPACITY;
-    int *perm = w.ints, *bidx = w.ints + w.nmax, *rank = bidx + 1024;
-    double *bsum = w.nrm + w.nmax, *bbest = bsum + 1024, *v = bbest + 1024, *scal = v + w.cmax;
+    int *perm = w.ints, *bidx = w.ints + w.nmax, *rank = bidx + 2048;
+    double *bsum = w.nrm + 2 * w.nmax, *bbest = bsum + 1024, *v = bbest + 1024, *scal = v + w.cmax;
     long tot = (long)n * c;
     transpose_init_kernel<<<ceil_div(tot, 256) < 2048 ? ceil_div(tot, 256) : 2048, 256, 0, s>>>(n, c, Z, w.M, perm);
     LYAP_TRY(launched());
-    static int max_blocks = 0;
+    const bool v2 = !env_flag("LYAP_RRQR_V1");
+    static int max_blocks = 0, max_blocks2 = 0;
     if (max_blocks == 0) {
-        int dev, nsm, per;
+        int dev, nsm, per, per2;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_kernel, 256, 0);
         max_blocks = nsm * (per < 2 ? per : 2);
         if (max_blocks > 1024) max_blocks = 1024;
         if (max_blocks < 1) max_blocks = 1;
+        cudaFuncSetAttribute(rrqr2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, rrqr2_kernel, 256, 48 * 1024);
+        max_blocks2 = nsm * std::max(1, std::min(per2, 1));
+        if (max_blocks2 > 512) max_blocks2 = 512;
     }
-    int want = ceil_div(n, 8);
-    int grid = want < max_blocks ? want : max_blocks;
-    RrqrArgs a{n, c, c < n ? c : n, tol, w.M, w.nrm, bsum, bbest, bidx, perm, v, scal, rank};
-    void *args[] = {&a};
-    LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)rrqr_kernel, dim3(grid), dim3(256), args, 0, s));
+    const int want = ceil_div(n, 8);
+    if (v2 && (size_t)c * sizeof(double) <= 160 * 1024) {
+        const int grid = std::max(1, std::min(want, max_blocks2));
+        Rrqr2Args a2{n, c, c < n ? c : n, tol, w.M, w.nrm, w.nrm + n, bsum, bbest, bidx, perm, w.ints + w.nmax + 2048 + 8,
+                     scal, rank};
+        void *args2[] = {&a2};
+        KTimer kt(KC_RRQR, s);
+        LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)rrqr2_kernel, dim3(grid), dim3(256), args2,
+                                                  sizeof(double) * (size_t)c, s));
+    } else {
+        const int grid = want < max_blocks ? want : max_blocks;
+        RrqrArgs a{n, c, c < n ? c : n, tol, w.M, w.nrm, bsum, bbest, bidx, perm, v, scal, rank};
+        void *args[] = {&a};
+        KTimer kt(KC_RRQR, s);
+        LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)rrqr_kernel, dim3(grid), dim3(256), args, 0, s));
+    }
     LYAP_TRY(launched());
     int k = 0;
     LYAP_CUDA_TRY(cudaMemcpyAsync(&k, rank, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -198,7 +386,10 @@ int rank_trunc_chol_f64(cudaStream_t s, int n, int c, const double *Z, double to
         return LYAP_OK;
     }
     long to = (long)n * k;
-    rrqr_out_kernel<<<ceil_div(to, 256) < 2048 ? ceil_div(to, 256) : 2048, 256, 0, s>>>(n, c, k, w.M, perm, prec_out, Zout);
+    if (v2 && (size_t)c * sizeof(double) <= 160 * 1024)
+        rrqr2_out_kernel<<<ceil_div(to, 256) < 2048 ? ceil_div(to, 256) : 2048, 256, 0, s>>>(n, c, k, w.M, prec_out, Zout);
+    else
+        rrqr_out_kernel<<<ceil_div(to, 256) < 2048 ? ceil_div(to, 256) : 2048, 256, 0, s>>>(n, c, k, w.M, perm, prec_out, Zout);
     LYAP_TRY(launched());
     *k_out = k;
     return LYAP_OK;

@@ -6,9 +6,13 @@ import paper_2510_02126_b200 as G
 import problems as P
 from bench import WORKLOADS
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg1"
-mc = int(sys.argv[2]) if len(sys.argv) > 2 else WORKLOADS[cfg]["max_cols"]
-wl = WORKLOADS[cfg]
-p = getattr(P, wl["gen"])()
+if cfg.startswith("cfg4"):                      # cfg4:<index> -- one member of the batched config
+    p = P.cfg4_member(int(cfg.split(":")[1]) if ":" in cfg else 0)
+    wl = dict(us="fp16", tol=1e-14, maxit=30, max_cols=1536)
+else:
+    wl = WORKLOADS[cfg]
+    p = getattr(P, wl["gen"])()
+mc = int(sys.argv[2]) if len(sys.argv) > 2 else wl["max_cols"]
 A = torch.tensor(p.A, dtype=torch.float64, device="cuda")
 Lt = torch.tensor(np.ascontiguousarray(p.L.T), dtype=torch.float64, device="cuda")
 S = torch.tensor(p.S, dtype=torch.float64, device="cuda") if p.S is not None else None
