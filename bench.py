@@ -305,10 +305,14 @@ def run_gpu(args):
             peak, unit, bound = pk["bf16_sus"], "TFLOP/s", "tensor"
             ach = flops / max(cnt, 1) / per_launch_s / 1e12
             src = pk["src"] + " bf16 sustained"
-        else:                      # latency-bound sequential kernels: report their memory rate
-            peak, unit, bound = pk["hbm"], "GB/s", "latency"
-            ach = nbytes / max(cnt, 1) / per_launch_s / 1e9
-            src = pk["src"] + " HBM (context only; the kernel is latency bound)"
+        else:                      # sequential (reflector / pivot chain) kernels: FMA work vs the ALU peak
+            # fp64 FMA peak = 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz = 37.2 TFLOP/s;
+            # the Gauss-Jordan panel runs in fp32 (128 FMA/clk/SM): 74.4 TFLOP/s
+            fma_per_clk = 128 if name == "gje_panel" else 64
+            peak, unit, bound = 148 * fma_per_clk * 2 * 1.965e9 / 1e12, "TFLOP/s", "alu"
+            ach = flops / max(cnt, 1) / per_launch_s / 1e12
+            src = (f"derived: 148 SMs x {fma_per_clk} FMA/clk x 2 x 1.965 GHz (DESIGN.md); the kernel is "
+                   "latency bound by its sequential reflector / pivot chain")
         return {"kernel": name, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
                 "frac": ach / peak if peak else None, "traffic": traffic_all.get(name),
                 "algorithmic_per_launch": (flops if unit == "TFLOP/s" else nbytes) / max(cnt, 1),

@@ -790,7 +790,9 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
         for (int k = K0; k < K0 + nbk; k += b0) {
             const int b = std::min(b0, K0 + nbk - k);
             {
-                KTimer kt(KC_GJE_PANEL, s);
+                // algorithmic work: panel LU ~ (n-k) b^2 flops + multiplier block X 2 n b^2
+                KTimer kt(KC_GJE_PANEL, s, (double)(n - k) * b * b + 2.0 * n * b * b,
+                          (double)sizeof(T) * ((double)(n - k) * b + (double)n * b));
                 LYAP_TRY(gje_panel_launch<T>(s, n, k, b, A, w));
             }
             LYAP_TRY(launched());
