@@ -125,8 +125,12 @@ def run_reference(args):
     import numpy as np
     import oracle
     import problems as P
-    wl = WORKLOADS[args.config]
-    p = getattr(P, wl["gen"])()
+    if args.config == "cfg4":
+        wl = dict(us="fp16", desc="configs[4] member 0 (n=2048 m=4 Cholesky fp16, kappa 10)")
+        p = P.cfg4_member(0)
+    else:
+        wl = WORKLOADS[args.config]
+        p = getattr(P, wl["gen"])()
     A = p.A
     oracle.lib()
     # warm-up: the full A-side sequence gives the number of inversions per solve
@@ -394,6 +398,110 @@ def sign_newton_scale(G, P, dev, pk, which):
     return res
 
 
+def run_batch(args):
+    """configs[4]: independent equations (n=2048, m=4, Cholesky, fp16), sharded over the
+    ranks; each rank solves --eq-per-gpu equations per step (a stratified sample over the
+    four kappa groups, different members on every rank), --lanes of them concurrently
+    (one host thread + solver handle + CUDA stream each)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2510_02126_b200 import batch as B
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    importlib_build()
+    import paper_2510_02126_b200 as G
+    import problems as P
+    E = args.eq_per_gpu
+    per_group = max(1, E // 4)
+    pool = B.stratified(256, 4, 64)                         # all 256, group-major
+    # weak scaling: rank r takes members r*per_group .. of every kappa group
+    idx = [g * 64 + (rank * per_group + i) % 64 for g in range(4) for i in range(per_group)][:E]
+    del pool
+    probs = [P.cfg4_member(i) for i in idx]
+    n = probs[0].n
+    lanes = max(1, min(args.lanes, E))
+    streams = [torch.cuda.Stream(device=dev) for _ in range(lanes)]
+    solvers = []
+    for ln in range(lanes):
+        with torch.cuda.stream(streams[ln]):
+            solvers.append(G.Solver(n, us="fp16", max_cols=args.max_cols))
+    dA = [torch.tensor(p.A, dtype=torch.float64, device=dev) for p in probs]
+    dL = [torch.tensor(np.ascontiguousarray(p.L.T), dtype=torch.float64, device=dev) for p in probs]
+    torch.cuda.synchronize()
+
+    def work(k, ln):
+        with torch.cuda.stream(streams[ln]):
+            r = solvers[ln].solve(dA[k], dL[k], None, tol=1e-14, maxit=30)
+        rep = r.report
+        return {"index": idx[k], "steps": rep["steps"], "res": rep["final_res"], "rank": rep["rank"],
+                "ok": 1.0 if rep["status"] == "converged" else 0.0}
+
+    items = list(range(E))
+    for k in items:                               # first warm-up pass sequential (one-time setup)
+        work(k, k % lanes)
+    for _ in range(args.warmup - 1):
+        B.run_concurrent(work, items, lanes)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = G.launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            results = B.run_concurrent(work, items, lanes)
+        torch.cuda.synchronize()
+        e1.record()
+        torch.cuda.synchronize()
+    launches = G.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    tmax = B.max_over_ranks(ms) if world > 1 else ms
+    allres = B.gather_results(results, ["index", "steps", "res", "rank", "ok"]) if world > 1 else results
+    # end to end: host (pinned) inputs, factors read back, same concurrency
+    hA = [torch.tensor(p.A).pin_memory().numpy() for p in probs]
+    hL = [torch.tensor(np.ascontiguousarray(p.L.T)).pin_memory().numpy() for p in probs]
+    ranks_h = []
+
+    def work_h(k, ln):
+        with torch.cuda.stream(streams[ln]):
+            Z, _, rep = solvers[ln].solve_host(hA[k], hL[k], None, tol=1e-14, maxit=30)
+        return {"rank": rep["rank"]}
+    t0 = time.perf_counter()
+    rh = B.run_concurrent(work_h, items, lanes)
+    te = time.perf_counter() - t0
+    te = B.max_over_ranks(te) if world > 1 else te
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    value = world * E * args.steps / (tmax / 1e3)
+    h2d = sum(8 * (n * n + n * p.m) for p in probs)
+    d2h = sum(8 * n * r["rank"] for r in rh)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tmax / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp16", "data": "synthetic",
+        "config": {"workload": f"configs[4] batch: n=2048 m=4 Cholesky fp16, {E} equations per GPU per step "
+                               f"(kappa groups 1e1..1e4), {lanes} concurrent solver handles/streams per GPU",
+                   "n": n, "equations_per_gpu": E, "lanes": lanes, "parallelism": f"dp{world}",
+                   "l2": "inputs (32 MB A per equation) exceed L2 together; no flush"},
+        "equations": allres, "all_converged": all(r["ok"] == 1.0 for r in allres),
+        "e2e": {"value": world * E / te, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def importlib_build():
     import importlib
     b = importlib.import_module("paper_2510_02126_b200.build")
@@ -406,8 +514,11 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="cfg1", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="cfg1", choices=sorted(WORKLOADS) + ["cfg4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eq-per-gpu", type=int, default=4, help="configs[4]: equations per GPU per step")
+    ap.add_argument("--lanes", type=int, default=4, help="configs[4]: concurrent solver handles per GPU")
+    ap.add_argument("--max-cols", type=int, default=1536, help="configs[4]: factor capacity per handle")
     ap.add_argument("--scale", default="cfg2", choices=["none", "cfg2", "cfg3"],
                     help="also time the fp16 sign-Newton A-sequence at this configuration's n (rank 0)")
     args = ap.parse_args()
@@ -415,6 +526,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "cfg4":
+        return run_batch(args)
     return run_gpu(args)
 
 

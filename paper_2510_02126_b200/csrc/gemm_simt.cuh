@@ -8,6 +8,8 @@
 // Skinny products (few output tiles, long K) are split along K into a
 // workspace and reduced in a fixed order (deterministic).
 #pragma once
+#include <mutex>
+#include <unordered_map>
 #include <type_traits>
 #include "common.cuh"
 #include "ktimer.h"
@@ -101,16 +103,20 @@ __global__ void splitk_reduce_kernel(int M, int N, int splits, const Acc *__rest
     }
 }
 
-// grow-only device workspace for split-K partials
-inline void *splitk_workspace(size_t bytes) {
-    static void *ptr = nullptr;
-    static size_t cap = 0;
-    if (bytes > cap) {
-        if (ptr) { cudaDeviceSynchronize(); cudaFree(ptr); }
-        cap = bytes + bytes / 2;
-        if (cudaMalloc(&ptr, cap) != cudaSuccess) { ptr = nullptr; cap = 0; }
+// grow-only device workspace for split-K partials, one per stream (concurrent solver
+// handles on different streams must not share it; growth synchronises only that stream)
+inline void *splitk_workspace(size_t bytes, cudaStream_t s) {
+    struct Buf { void *ptr = nullptr; size_t cap = 0; };
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, Buf> bufs;
+    std::lock_guard<std::mutex> lock(mu);
+    Buf &b = bufs[s];
+    if (bytes > b.cap) {
+        if (b.ptr) { cudaStreamSynchronize(s); cudaFree(b.ptr); }
+        b.cap = bytes + bytes / 2;
+        if (cudaMalloc(&b.ptr, b.cap) != cudaSuccess) { b.ptr = nullptr; b.cap = 0; }
     }
-    return ptr;
+    return b.ptr;
 }
 
 // ---------------------------------------------------------------- fp64 on the DMMA pipe
@@ -229,7 +235,7 @@ int gemm_strided(cudaStream_t s, int M, int N, int K, Acc alpha,
     if (K <= 0) splits = 1;
     Acc *work = nullptr;
     if (splits > 1) {
-        work = (Acc *)splitk_workspace(sizeof(Acc) * (size_t)splits * M * N);
+        work = (Acc *)splitk_workspace(sizeof(Acc) * (size_t)splits * M * N, s);
         if (!work) splits = 1;
     }
     const int kchunk = (splits > 1) ? ceil_div(ceil_div(K, splits), BK) * BK : std::max(K, 1);

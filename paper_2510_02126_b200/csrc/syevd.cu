@@ -92,11 +92,13 @@ tridiag_kernel(TridArgs a)
     if (blockIdx.x == 0 && threadIdx.x == 0) a.d[0] = A[0];
     grid.sync();
     for (int j = 0; j + 2 < p; j++) {
+        const double *Pc = a.P + (long)(j & 1) * p;             // P double-buffered by step parity
+        double *Pn = a.P + (long)((j + 1) & 1) * p;
         const int L = p - j - 1;                 // rows j+1 .. p-1
         const int r0 = j + 1;
         // (c) w = P - (tau/2)(P.v) v     (all CTAs, identical)
         double k = 0.0;
-        for (int i = threadIdx.x; i < L; i += blockDim.x) { double t = a.P[r0 + i]; w[i] = t; k = fma(t, v[i], k); }
+        for (int i = threadIdx.x; i < L; i += blockDim.x) { double t = Pc[r0 + i]; w[i] = t; k = fma(t, v[i], k); }
         k = 0.5 * tau * block_sum(k, red);
         for (int i = threadIdx.x; i < L; i += blockDim.x) w[i] = fma(-k, v[i], w[i]);
         __syncthreads();
@@ -127,7 +129,7 @@ tridiag_kernel(TridArgs a)
             }
             if (more) {
                 s = warp_sum(s);
-                if (lane == 0) a.P[g] = taun * s;
+                if (lane == 0) Pn[g] = taun * s;
             }
         }
         grid.sync();
@@ -173,9 +175,11 @@ tridiag_reg_kernel(TridArgs a)
     if (blockIdx.x == 0 && threadIdx.x == 0) a.d[0] = A[0];
     grid.sync();
     for (int j = 0; j + 2 < p; j++) {
+        const double *Pc = a.P + (long)(j & 1) * p;             // P double-buffered by step parity
+        double *Pn = a.P + (long)((j + 1) & 1) * p;
         const int L = p - j - 1, r0 = j + 1;
         double k = 0.0;
-        for (int i = threadIdx.x; i < L; i += blockDim.x) { double t = a.P[r0 + i]; w[i] = t; k = fma(t, v[i], k); }
+        for (int i = threadIdx.x; i < L; i += blockDim.x) { double t = Pc[r0 + i]; w[i] = t; k = fma(t, v[i], k); }
         k = 0.5 * tau * block_sum(k, red);
         for (int i = threadIdx.x; i < L; i += blockDim.x) w[i] = fma(-k, v[i], w[i]);
         __syncthreads();
@@ -207,7 +211,7 @@ tridiag_reg_kernel(TridArgs a)
             }
             if (more) {
                 s = warp_sum(s);
-                if (lane == 0) a.P[g] = taun * s;
+                if (lane == 0) Pn[g] = taun * s;
             }
             if (g == r0 + 1) {                  // publish column j+2 for the next step
 #pragma unroll
@@ -285,6 +289,10 @@ tridiag_w_kernel(TridArgs a)
 #endif
     for (int j = 0; j + 2 < p; j++) {
         const int cur = j & 1, nxt = cur ^ 1;
+        // P is double-buffered by step parity: a fast CTA's owners publish P for step j+1
+        // while a slower CTA may still be reading step j's P
+        const double *Pc = a.P + (long)cur * p;
+        double *Pn = a.P + (long)nxt * p;
         const int r0 = j + 1;
         const double *v = vb[cur];
         double *vn = vb[nxt];
@@ -298,7 +306,7 @@ tridiag_w_kernel(TridArgs a)
         const double *cj = A + (long)r0 * p;
         double pv = 0.0, yy = 0.0, yv = 0.0, vv = 0.0;
         for (int i = r0 + threadIdx.x; i < p; i += blockDim.x) {
-            const double Pi = a.P[i], vi = v[i], yi = cj[i] - Pi;
+            const double Pi = Pc[i], vi = v[i], yi = cj[i] - Pi;
             w[i] = Pi;
             vn[i] = yi;
             pv = fma(Pi, vi, pv);
@@ -306,8 +314,8 @@ tridiag_w_kernel(TridArgs a)
         }
         pv = warp_sum(pv); yy = warp_sum(yy); yv = warp_sum(yv); vv = warp_sum(vv);
         if (lane == 0) { red1[wid] = pv; red1[8 + wid] = yy; red1[16 + wid] = yv; red2[wid] = vv; }
-        const double P0 = a.P[r0], y0 = cj[r0] - P0;
-        const double P1 = (r0 + 1 < p) ? a.P[r0 + 1] : 0.0, y1 = (r0 + 1 < p) ? cj[r0 + 1] - P1 : 0.0;
+        const double P0 = Pc[r0], y0 = cj[r0] - P0;
+        const double P1 = (r0 + 1 < p) ? Pc[r0 + 1] : 0.0, y1 = (r0 + 1 < p) ? cj[r0 + 1] - P1 : 0.0;
         TPROF(0);
         __syncthreads();
         TPROF(1);
@@ -366,7 +374,7 @@ tridiag_w_kernel(TridArgs a)
             }
             if (more) {
                 ss = warp_sum(ss);
-                if (lane == 0) a.P[g] = s_tau[nxt] * ss;
+                if (lane == 0) Pn[g] = s_tau[nxt] * ss;
             }
             if (g == r0 + 1) {
 #pragma unroll
