@@ -274,8 +274,11 @@ int thin_qr_F(lyap_ir_ctx *h, int p, int c_orth) {
     const int n = h->n;
     cudaStream_t s = h->s;
     const int c = c_orth, q = p - c;
-    // fast path only with ample room (p <= n/2) and a well-conditioned remainder
-    if (!h->zorth || c <= 0 || q <= 0 || 2 * p > n) return qr_f64(s, n, p, h->F, h->U, h->Tm, h->qr);
+    // fast path with ample room (p <= n/2: the projected block is rarely rank deficient
+    // there; near convergence [Z, AZ, L] is numerically rank deficient and the unpivoted
+    // Householder completion would not stay orthogonal to Z); the result is verified
+    if (!h->zorth || c <= 0 || q <= 0 || 2 * p > n || env_flag("LYAP_NO_BCGS"))
+        return qr_f64(s, n, p, h->F, h->U, h->Tm, h->qr);
     const double *Z = h->F;
     double *B = h->F + (size_t)n * c;
     double *X1 = h->TN, *X2 = h->Hm, *R2 = h->Vs;
@@ -287,12 +290,16 @@ int thin_qr_F(lyap_ir_ctx *h, int p, int c_orth) {
     LYAP_TRY(nk_axpy(s, (long)c * q, 1.0, X2, X1));          // Rz = X1 + X2
     const int k2 = std::min(n - c, q);
     LYAP_TRY(qr_f64(s, n, q, B, h->U + (size_t)n * c, R2, h->qr));
-    // |diag(R2)| range: a near-zero pivot would leave an arbitrary (non-orthogonal to Z)
-    // Householder completion column -> fall back to the full Householder QR
+    // checks: |diag(R2)| range (a near-zero pivot leaves an arbitrary Householder
+    // completion column) and ||Z^T Q2||_F (the completion must stay orthogonal to Z)
     LYAP_TRY(nk_diag_range(s, k2, R2, k2, h->scal + SC_TR));
+    LYAP_TRY(dgemm_cm(s, true, false, c, k2, n, 1.0, Z, n, h->U + (size_t)n * c, n, 0.0, X2, c));
+    LYAP_TRY(nk_sumsq(s, (long)c * k2, X2, h->scal + SC_ORTH));
     LYAP_TRY(sync_read(h, h->hscal, h->scal, sizeof(double) * SC_COUNT));
-    const double dmin = h->hscal[SC_TR], dmax = h->hscal[SC_TR + 1];
-    if (!(dmin >= 1e-6 * dmax)) {
+    const double dmin = h->hscal[SC_TR], dmax = h->hscal[SC_TR + 1], e2 = h->hscal[SC_ORTH];
+    if (!(dmin >= 1e-6 * dmax) || !(e2 <= 1e-24)) {
+        if (verbose()) fprintf(stderr, "lyap:   BCGS fast path rejected (dmin/dmax %.2e, ||Z^T Q2|| %.2e)\n",
+                               dmax > 0 ? dmin / dmax : 0.0, std::sqrt(e2));
         LYAP_TRY(nk_copy_block(s, n, q, h->Zd2, n, B, n, 1.0));
         return qr_f64(s, n, p, h->F, h->U, h->Tm, h->qr);
     }

@@ -17,6 +17,7 @@ enum {
     SC_TR = 11,      // trace results (norms of implied products)
     SC_TR2 = 12,
     SC_MAXB = 13,    // scratch: bit pattern of a grid-wide max|x| (atomicMax on non-negative doubles)
+    SC_ORTH = 14,    // ||Z^T Q2||_F^2 of the block Gram-Schmidt fast path
     SC_COUNT = 16
 };
 
