@@ -237,7 +237,7 @@ tridiag_reg_kernel(TridArgs a)
 // column j+1 after step j, the next reflector vn) in shared memory; the owners then
 // update their register-resident columns and publish P[g] = tau_{j+1} (col_g . vn).
 // Same arithmetic as tridiag_reg_kernel up to the reduction trees.
-template <int CH>
+template <int CH, int CPW>
 __global__ void __launch_bounds__(256)
 tridiag_w_kernel(TridArgs a)
 {
@@ -249,14 +249,18 @@ tridiag_w_kernel(TridArgs a)
     __shared__ double s_tau[2], s_beta[2];
     __shared__ double red1[32], red2[32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
-    const int g = blockIdx.x * nwb + wid;
-    const bool owner = g < p;
+    // warp gw owns columns gw + t * nwg (t < CPW): fewer CTAs -> a cheaper grid barrier
+    const int gw = blockIdx.x * nwb + wid, nwg = gridDim.x * nwb;
     double *A = a.A;
-    double col[CH];
+    double col[CPW][CH];
 #pragma unroll
-    for (int u = 0; u < CH; u++) {
-        const int i = lane + 32 * u;
-        col[u] = (owner && i < p) ? A[(long)g * p + i] : 0.0;
+    for (int t = 0; t < CPW; t++) {
+        const int g = gw + t * nwg;
+#pragma unroll
+        for (int u = 0; u < CH; u++) {
+            const int i = lane + 32 * u;
+            col[t][u] = (g < p && i < p) ? A[(long)g * p + i] : 0.0;
+        }
     }
     // reflector 0 from column 0, rows 1.. (warp 0 of every CTA)
     if (wid == 0) {
@@ -272,13 +276,17 @@ tridiag_w_kernel(TridArgs a)
         if (blockIdx.x == 0 && lane == 0) a.d[0] = A[0];
     }
     __syncthreads();
-    if (owner && g >= 1) {
-        const double *v = vb[0];
-        double ss = 0.0;
 #pragma unroll
-        for (int u = 0; u < CH; u++) { const int i = lane + 32 * u; if (i >= 1 && i < p) ss = fma(col[u], v[i], ss); }
-        ss = warp_sum(ss);
-        if (lane == 0) a.P[g] = s_tau[0] * ss;
+    for (int t = 0; t < CPW; t++) {
+        const int g = gw + t * nwg;
+        if (g < p && g >= 1) {
+            const double *v = vb[0];
+            double ss = 0.0;
+#pragma unroll
+            for (int u = 0; u < CH; u++) { const int i = lane + 32 * u; if (i >= 1 && i < p) ss = fma(col[t][u], v[i], ss); }
+            ss = warp_sum(ss);
+            if (lane == 0) a.P[g] = s_tau[0] * ss;
+        }
     }
     grid.sync();
 #ifdef LYAP_PANEL_PROF
@@ -360,32 +368,36 @@ tridiag_w_kernel(TridArgs a)
         }
         __syncthreads();
         TPROF(3);
-        if (owner && g >= r0 + 1) {
-            const double vg = v[g], wg = w[g];
-            double ss = 0.0;
 #pragma unroll
-            for (int u = 0; u < CH; u++) {
-                const int i = lane + 32 * u;
-                if (i >= r0 + 1 && i < p) {
-                    const double x = col[u] - v[i] * wg - w[i] * vg;
-                    col[u] = x;
-                    if (more) ss = fma(x, vn[i], ss);
-                }
-            }
-            if (more) {
-                ss = warp_sum(ss);
-                if (lane == 0) Pn[g] = s_tau[nxt] * ss;
-            }
-            if (g == r0 + 1) {
+        for (int t = 0; t < CPW; t++) {
+            const int g = gw + t * nwg;
+            if (g < p && g >= r0 + 1) {
+                const double vg = v[g], wg = w[g];
+                double ss = 0.0;
 #pragma unroll
                 for (int u = 0; u < CH; u++) {
                     const int i = lane + 32 * u;
-                    if (i >= r0 + 1 && i < p) A[(long)g * p + i] = col[u];
+                    if (i >= r0 + 1 && i < p) {
+                        const double x = col[t][u] - v[i] * wg - w[i] * vg;
+                        col[t][u] = x;
+                        if (more) ss = fma(x, vn[i], ss);
+                    }
                 }
-            }
-            if (g == p - 1 && !more) {
+                if (more) {
+                    ss = warp_sum(ss);
+                    if (lane == 0) Pn[g] = s_tau[nxt] * ss;
+                }
+                if (g == r0 + 1) {
 #pragma unroll
-                for (int u = 0; u < CH; u++) if (lane + 32 * u == p - 1) a.d[p - 1] = col[u];
+                    for (int u = 0; u < CH; u++) {
+                        const int i = lane + 32 * u;
+                        if (i >= r0 + 1 && i < p) A[(long)g * p + i] = col[t][u];
+                    }
+                }
+                if (g == p - 1 && !more) {
+#pragma unroll
+                    for (int u = 0; u < CH; u++) if (lane + 32 * u == p - 1) a.d[p - 1] = col[t][u];
+                }
             }
         }
         TPROF(4);
@@ -1039,19 +1051,23 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
                 cudaFuncSetAttribute(tridiag_reg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
                 cudaFuncSetAttribute(tridiag_reg_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
                 cudaFuncSetAttribute(tridiag_reg_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                cudaFuncSetAttribute(tridiag_w_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                cudaFuncSetAttribute(tridiag_w_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                cudaFuncSetAttribute(tridiag_w_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                cudaFuncSetAttribute(tridiag_w_kernel<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                cudaFuncSetAttribute(tridiag_w_kernel<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                cudaFuncSetAttribute(tridiag_w_kernel<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
                 attr2 = true;
             }
             void *fn;
-            if (env_flag("LYAP_TRIDIAG_REG"))
+            int grid_t = need;
+            if (env_flag("LYAP_TRIDIAG_REG")) {
                 fn = (p <= 256) ? (void *)tridiag_reg_kernel<8>
                    : (p <= 512) ? (void *)tridiag_reg_kernel<16> : (void *)tridiag_reg_kernel<32>;
-            else
-                fn = (p <= 256) ? (void *)tridiag_w_kernel<8>
-                   : (p <= 512) ? (void *)tridiag_w_kernel<16> : (void *)tridiag_w_kernel<32>;
-            LYAP_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(need), dim3(256), args, smem, s));
+            } else {
+                // one column per warp (two per warp measured slower: the owners' update is on
+                // the critical path of every step, the grid barrier is not cheaper enough)
+                fn = (p <= 256) ? (void *)tridiag_w_kernel<8, 1>
+                   : (p <= 512) ? (void *)tridiag_w_kernel<16, 1> : (void *)tridiag_w_kernel<32, 1>;
+            }
+            LYAP_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid_t), dim3(256), args, smem, s));
         } else {
             int grid = std::min(max_blocks, std::max(1, p / 4));
             LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)tridiag_kernel, dim3(grid), dim3(256), args, smem, s));
