@@ -130,19 +130,19 @@ __device__ __forceinline__ void dmma8x8x4(double &d0, double &d1, double a, doub
                  : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
-static __global__ void __launch_bounds__(128)
-dgemm_dmma_kernel(int M, int N, int K, int kchunk, double alpha,
-                  const double *__restrict__ A, long sam, long sak,
-                  const double *__restrict__ B, long sbk, long sbn,
-                  double beta, double *__restrict__ C, long scm, long scn, double *__restrict__ work)
+// one 64 x 64 tile of C = alpha A B (+ beta C), k range [kb, ke); 128 threads.  work != 0:
+// write the split-K partial to work + wz instead (M x N, column-major)
+__device__ __forceinline__ void dmma_tile(int M, int N, int kb, int ke, long m0, long n0, double alpha,
+                                          const double *__restrict__ A, long sam, long sak,
+                                          const double *__restrict__ B, long sbk, long sbn,
+                                          double beta, double *__restrict__ C, long scm, long scn,
+                                          double *__restrict__ work, long wz)
 {
     constexpr int BM = 64, BN = 64, BK = 16, PAD = 4;
     __shared__ double As[2][BK][BM + PAD];
     __shared__ double Bs[2][BK][BN + PAD];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-    const long m0 = (long)blockIdx.y * BM, n0 = (long)blockIdx.x * BN;
-    const int kb = blockIdx.z * kchunk, ke = min(K, kb + kchunk);
     const bool a_kfast = (sak == 1), b_kfast = (sbk == 1);
     double acc[4][4][2];
 #pragma unroll
@@ -208,13 +208,24 @@ dgemm_dmma_kernel(int M, int N, int K, int kchunk, double alpha,
                 const long gn = n0 + wn + j * 8 + 2 * lk + v;
                 if (gn >= N) continue;
                 const double r = alpha * acc[i][j][v];
-                if (work) work[(long)blockIdx.z * M * N + gm + gn * (long)M] = r;
+                if (work) work[wz + gm + gn * (long)M] = r;
                 else {
                     double *cp = C + gm * scm + gn * scn;
                     *cp = (beta != 0.0) ? fma(beta, *cp, r) : r;
                 }
             }
     }
+}
+
+static __global__ void __launch_bounds__(128)
+dgemm_dmma_kernel(int M, int N, int K, int kchunk, double alpha,
+                  const double *__restrict__ A, long sam, long sak,
+                  const double *__restrict__ B, long sbk, long sbn,
+                  double beta, double *__restrict__ C, long scm, long scn, double *__restrict__ work)
+{
+    const int kb = blockIdx.z * kchunk, ke = min(K, kb + kchunk);
+    dmma_tile(M, N, kb, ke, (long)blockIdx.y * 64, (long)blockIdx.x * 64, alpha, A, sam, sak, B, sbk, sbn, beta, C,
+              scm, scn, work, (long)blockIdx.z * M * N);
 }
 
 template <typename TA, typename TB, typename TC, typename Acc>

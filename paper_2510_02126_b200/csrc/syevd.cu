@@ -591,6 +591,18 @@ dc_leaf_kernel(int p, const int *__restrict__ bounds, const double *__restrict__
 
 struct MergeInfo { int lo, mid, hi; };
 
+__global__ void dc_tear_kernel(int nl, const int *__restrict__ bounds, const double *__restrict__ e,
+                               double *__restrict__ d)
+{
+    const int i = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nl) {
+        const int m = bounds[i];
+        const double r = fabs(e[m - 1]);
+        d[m - 1] -= r;
+        d[m] -= r;
+    }
+}
+
 // M1: z, sort, deflation scan.  One CTA per merge.
 //   out (per merge, indexed from lo): perm (sorted position -> local column),
 //   Ds (sorted, deflation-modified), zK/DK (non-deflated compressed), K (positions),
@@ -824,6 +836,21 @@ __global__ void dc_umatrix_kernel(int p, const MergeInfo *__restrict__ mi, const
         const double inv = 1.0 / sqrt(ss);
         for (int i = lane; i < kk; i += 32) U[(long)(lo + j) * p + lo + i] *= inv;
     }
+}
+
+// M5: Qn = Qk U for every merge of the level in one launch (grid.z = merge), sizes read on
+// the device (no host synchronisation): rows n_q = hi - lo, kk_q = counts[2q] non-deflated
+// columns, fp64 DMMA tiles of 64 x 64.
+static __global__ void __launch_bounds__(128)
+dc_gemm_grouped_kernel(int p, const MergeInfo *__restrict__ mi, const int *__restrict__ counts,
+                       const double *__restrict__ Qk, const double *__restrict__ U, double *__restrict__ Qn)
+{
+    const MergeInfo m = mi[blockIdx.z];
+    const int n = m.hi - m.lo, kk = counts[2 * blockIdx.z];
+    const long m0 = (long)blockIdx.y * 64, n0 = (long)blockIdx.x * 64;
+    if (kk <= 0 || m0 >= n || n0 >= kk) return;
+    const size_t off = (size_t)m.lo * p + m.lo;
+    dmma_tile(n, kk, 0, kk, m0, n0, 1.0, Qk + off, 1, p, U + off, 1, p, 0.0, Qn + off, 1, p, nullptr, 0);
 }
 
 // M6: eigenvalues of the merged block and assembly of the (unsorted) columns:
@@ -1080,18 +1107,13 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
     while ((p + nl - 1) / nl > 32) nl *= 2;
     std::vector<int> hb(nl + 1);
     for (int i = 0; i <= nl; i++) hb[i] = (int)((long)i * p / nl);
-    std::vector<double> hd(p), he(std::max(p - 1, 1));
-    LYAP_CUDA_TRY(cudaMemcpyAsync(hd.data(), d, sizeof(double) * p, cudaMemcpyDeviceToHost, s));
-    if (p > 1) LYAP_CUDA_TRY(cudaMemcpyAsync(he.data(), e, sizeof(double) * (p - 1), cudaMemcpyDeviceToHost, s));
-    LYAP_CUDA_TRY(cudaStreamSynchronize(s));
-    for (int i = 1; i < nl; i++) {          // Cuppen tears: T = diag(T1', T2') + |e| v v^T
-        int m = hb[i];
-        double r = fabs(he[m - 1]);
-        hd[m - 1] -= r;
-        hd[m] -= r;
-    }
-    LYAP_CUDA_TRY(cudaMemcpyAsync(d, hd.data(), sizeof(double) * p, cudaMemcpyHostToDevice, s));
+    // Cuppen tears T = diag(T1', T2') + |e| v v^T at the leaf boundaries, on the device
+    // (leaves are >= 16 long, so no two tears touch the same diagonal entry)
     LYAP_CUDA_TRY(cudaMemcpyAsync(bounds, hb.data(), sizeof(int) * (nl + 1), cudaMemcpyHostToDevice, s));
+    if (nl > 1) {
+        dc_tear_kernel<<<ceil_div(nl, 128), 128, 0, s>>>(nl, bounds, e, d);
+        LYAP_TRY(launched());
+    }
     zero_d_kernel<<<gsz, 256, 0, s>>>((long)pp, W.Q);
     LYAP_TRY(launched());
     dc_leaf_kernel<<<nl, 256, 0, s>>>(p, bounds, d, e, lam, W.Q);
@@ -1124,15 +1146,11 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
         dim3 g2(ceil_div((long)maxn * 32, 256), nm);
         dc_umatrix_kernel<<<g2, 256, 0, s>>>(p, mi, DK, counts, taus, orig, zhat, W.U);
         LYAP_TRY(launched());
-        std::vector<int> hc(2 * nm);
-        LYAP_CUDA_TRY(cudaMemcpyAsync(hc.data(), counts, sizeof(int) * 2 * nm, cudaMemcpyDeviceToHost, s));
-        LYAP_CUDA_TRY(cudaStreamSynchronize(s));
-        for (int q = 0; q < nm; q++) {
-            const int lo = hm[q].lo, n = hm[q].hi - hm[q].lo, kk = hc[2 * q];
-            if (kk > 0) {
-                const size_t off = (size_t)lo * p + lo;
-                LYAP_TRY(dgemm_cm(s, false, false, n, kk, kk, 1.0, W.Qk + off, p, W.U + off, p, 0.0, W.Qn + off, p));
-            }
+        {
+            const dim3 gg(ceil_div(maxn, 64), ceil_div(maxn, 64), nm);
+            KTimer kt(KC_DGEMM, s);
+            dc_gemm_grouped_kernel<<<gg, 128, 0, s>>>(p, mi, counts, W.Qk, W.U, W.Qn);
+            LYAP_TRY(launched());
         }
         dc_finish_kernel<<<g1, 128, 0, s>>>(p, mi, Ds, DK, counts, taus, orig, Dpos, W.Qg, W.Qn, lamtmp);
         LYAP_TRY(launched());
