@@ -763,22 +763,31 @@ __global__ void dc_secular_kernel(const MergeInfo *__restrict__ mi, const double
         double a, b;                          // tau interval
         if (o == j) { a = 0.0; b = (j + 1 < kk) ? 0.5 * (du - dl) : du - dl; }
         else { a = -(0.5 * (du - dl)); b = 0.0; }
-        // safeguarded Newton on f(tau) = 1 + rho sum z_i^2 / (delta_i - tau), f increasing on
-        // (a, b): the bracket shrinks with the sign of f, Newton steps leaving it are
-        // replaced by bisection; stop at a relative step of 2 ulp or a collapsed bracket
-        double tau = 0.5 * (a + b);
+        // Newton on h(tau) = (delta_o - tau) f(tau) = rho z_o^2 - tau (1 + rho S(tau)),
+        // S = sum_{i != o} z_i^2 / (delta_i - tau): the pole at the origin is removed, so the
+        // iteration converges fast for roots close to it (the usual case after deflation).
+        // Started at tau = 0 (first step = the one-pole estimate rho z_o^2 / (1 + rho S(0))),
+        // safeguarded by the bracket (a, b) of f's sign change and bisection.
+        const double zo2 = rho * z[o] * z[o];
+        double tau = 0.0;
         for (int it = 0; it < 200; it++) {
-            double f = 0.0, df = 0.0;
+            double S = 0.0, dS = 0.0;
             for (int i = lane; i < kk; i += 32) {
+                if (i == o) continue;
                 const double t = z[i] / ((D[i] - Do) - tau);
-                f = fma(t, z[i], f);
-                df = fma(t, t, df);
+                S = fma(t, z[i], S);
+                dS = fma(t, t, dS);
             }
-            f = 1.0 + rho * warp_sum(f);
-            df = rho * warp_sum(df);
-            if (f == 0.0) break;
-            if (f > 0.0) b = tau; else a = tau;
-            double tn = tau - f / df;
+            S = rho * warp_sum(S);
+            dS = rho * warp_sum(dS);
+            const double h = zo2 - tau * (1.0 + S);
+            const double dh = -(1.0 + S) - tau * dS;
+            if (tau != 0.0) {
+                if (h == 0.0) break;
+                const double fs = (o == j) ? -h : h;             // sign of f (f increasing)
+                if (fs > 0.0) b = tau; else a = tau;
+            }
+            double tn = (dh != 0.0) ? tau - h / dh : 0.5 * (a + b);
             if (!(tn > a && tn < b)) tn = 0.5 * (a + b);
             const bool done = (tn == a || tn == b || fabs(tn - tau) <= 4.4e-16 * fabs(tn));
             tau = tn;
