@@ -55,6 +55,9 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
         :: "r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, const void *src, int c0, int c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
                  :: "l"(map), "r"(smem_u32(src)), "r"(c0), "r"(c1) : "memory");
@@ -242,6 +245,171 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(BN));
 }
 
+// ---------------------------------------------------------------- persistent variant
+// One CTA per SM loops over 128 x 128 output tiles (row-major C via TMA); warp-specialised:
+//   warp 0 (one lane)  TMA producer: the C tile of the tile (when blended) into one of two
+//                      C buffers, then the K blocks into the 4-stage A/B ring;
+//   warp 1 (one lane)  tcgen05.mma issuer into one of two TMEM accumulators (256 columns);
+//   warps 2-5          epilogue: TMEM -> registers -> blend with C in 128B-swizzled shared
+//                      memory -> TMA store; it frees the accumulator as soon as it has been
+//                      read, so the MMAs of tile i+1 overlap the epilogue of tile i.
+// Barriers: full/empty (A/B ring), acc_full/acc_empty (accumulators), c_full/c_empty (C).
+namespace tc {
+constexpr int PSTAGES = 4, PTHREADS = 192;
+constexpr int PSMEM = PSTAGES * (A_STAGE + B_STAGE) + 2 * C_STAGE + 1024 + 512;
+}  // namespace tc
+
+template <typename T>
+__global__ void __launch_bounds__(tc::PTHREADS, 1)
+tc_gemm_persistent_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmC, int M, int N, int K, float alpha, float beta)
+{
+    using namespace tc;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *base = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char *sA = base;
+    unsigned char *sB = sA + PSTAGES * A_STAGE;
+    unsigned char *sC = sB + PSTAGES * B_STAGE;                 // 2 x C_STAGE
+    uint64_t *full = (uint64_t *)(sC + 2 * C_STAGE);
+    uint64_t *empty = full + PSTAGES;
+    uint64_t *acc_full = empty + PSTAGES;
+    uint64_t *acc_empty = acc_full + 2;
+    uint64_t *c_full = acc_empty + 2;
+    uint64_t *c_empty = c_full + 2;
+    uint32_t *tmem_slot = (uint32_t *)(c_empty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tiles_n = (N + BN - 1) / BN, tiles = tiles_n * ((M + BM - 1) / BM);
+    const int nk = (K + BK - 1) / BK;
+    const bool blend = (beta != 0.f);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < PSTAGES; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], 4);            // one arrival per epilogue warp
+            mbar_init(&c_full[i], 1);
+            mbar_init(&c_empty[i], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" :: "l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" :: "l"(&tmB) : "memory");
+        asm volatile("prefetch.tensormap [%0];" :: "l"(&tmC) : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(tmem_slot)), "r"(2 * BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int kc = 0;
+            for (int t = blockIdx.x, i = 0; t < tiles; t += gridDim.x, i++) {
+                const int m0 = (t / tiles_n) * BM, n0 = (t % tiles_n) * BN, ab = i & 1;
+                if (blend) {
+                    if (i >= 2) mbar_wait(&c_empty[ab], ((i >> 1) - 1) & 1);
+                    mbar_expect_tx(&c_full[ab], C_STAGE);
+                    for (int w = 0; w < 4; w++)
+                        for (int hh = 0; hh < 2; hh++)
+                            tma_load_2d(sC + ab * C_STAGE + (w * 2 + hh) * 4096, &tmC, &c_full[ab], n0 + 64 * hh,
+                                        m0 + 32 * w);
+                }
+                for (int kb = 0; kb < nk; kb++, kc++) {
+                    const int st = kc % PSTAGES;
+                    if (kc >= PSTAGES) mbar_wait(&empty[st], ((kc / PSTAGES) - 1) & 1);
+                    mbar_expect_tx(&full[st], A_STAGE + B_STAGE);
+                    tma_load_2d(sA + st * A_STAGE, &tmA, &full[st], kb * BK, m0);
+                    tma_load_2d(sB + st * B_STAGE, &tmB, &full[st], kb * BK, n0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+            const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                   ((uint32_t)(BM >> 4) << 24);
+            int kc = 0;
+            for (int t = blockIdx.x, i = 0; t < tiles; t += gridDim.x, i++) {
+                const int ab = i & 1;
+                if (i >= 2) mbar_wait(&acc_empty[ab], ((i >> 1) - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t acc = tmem + (uint32_t)(ab * BN);
+                for (int kb = 0; kb < nk; kb++, kc++) {
+                    const int st = kc % PSTAGES;
+                    mbar_wait(&full[st], (kc / PSTAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint64_t da = smem_desc(sA + st * A_STAGE), db = smem_desc(sB + st * B_STAGE);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; k++)
+                        mma_f16(acc, da + 2 * k, db + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                    mma_commit(&empty[st]);
+                }
+                mma_commit(&acc_full[ab]);
+            }
+        }
+    } else {
+        // ---- epilogue warps 2..5; TMEM lane quarter = warp % 4
+        const int q4 = warp & 3;
+        for (int t = blockIdx.x, i = 0; t < tiles; t += gridDim.x, i++) {
+            const int m0 = (t / tiles_n) * BM, n0 = (t % tiles_n) * BN, ab = i & 1;
+            unsigned char *wbox = sC + ab * C_STAGE + q4 * 2 * 4096;
+            if (!blend && i >= 2) {
+                // the previous TMA store out of this buffer must have read it
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
+            }
+            mbar_wait(&acc_full[ab], (i >> 1) & 1);
+            if (blend) mbar_wait(&c_full[ab], (i >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+                float v[16];
+                tmem_ld16(tmem + (uint32_t)(ab * BN) + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0, v);
+                unsigned char *rowp = wbox + (c0 >> 6) * 4096 + lane * 128;
+                const int j0 = (c0 & 63) >> 3;
+                uint4 *p0 = reinterpret_cast<uint4 *>(rowp + (((j0) ^ (lane & 7)) << 4));
+                uint4 *p1 = reinterpret_cast<uint4 *>(rowp + (((j0 + 1) ^ (lane & 7)) << 4));
+                alignas(16) T o[16];
+                if (blend) {
+                    alignas(16) T ci[16];
+                    *reinterpret_cast<uint4 *>(ci) = *p0;
+                    *reinterpret_cast<uint4 *>(ci + 8) = *p1;
+#pragma unroll
+                    for (int e = 0; e < 16; e++) o[e] = from_f<T>(fmaf(beta, to_f<T>(ci[e]), alpha * v[e]));
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 16; e++) o[e] = from_f<T>(alpha * v[e]);
+                }
+                *p0 = *reinterpret_cast<const uint4 *>(o);
+                *p1 = *reinterpret_cast<const uint4 *>(o + 8);
+            }
+            // accumulator read: let the MMA warp reuse it
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_2d(&tmC, wbox, n0, m0 + 32 * q4);
+                tma_store_2d(&tmC, wbox + 4096, n0 + 64, m0 + 32 * q4);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                if (blend) {
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    mbar_arrive(&c_empty[ab]);
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        __syncwarp();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(2 * BN));
+}
+
 // ---------------------------------------------------------------- host side
 namespace {
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -299,6 +467,23 @@ int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const vo
         attr = true;
     }
     KTimer kt(KC_TCGEMM, s, 2.0 * M * N * K, 2.0 * ((double)M * K + (double)N * K + (beta != 0.f ? 2.0 : 1.0) * M * N));
+    static int nsm = 0;
+    if (nsm == 0) {
+        int dev;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(tc_gemm_persistent_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::PSMEM);
+        cudaFuncSetAttribute(tc_gemm_persistent_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::PSMEM);
+    }
+    const int tiles = (int)(grid.x * grid.y);
+    if (ctma && tiles >= nsm && !env_flag("LYAP_TC_NONPERSISTENT")) {
+        const int g = std::min(tiles, nsm);
+        if (prec == LYAP_BF16)
+            tc_gemm_persistent_kernel<__nv_bfloat16><<<g, tc::PTHREADS, tc::PSMEM, s>>>(ma, mb, mc, M, N, K, alpha, beta);
+        else
+            tc_gemm_persistent_kernel<__half><<<g, tc::PTHREADS, tc::PSMEM, s>>>(ma, mb, mc, M, N, K, alpha, beta);
+        return launched();
+    }
     if (prec == LYAP_BF16)
         tc_gemm_kernel<__nv_bfloat16><<<grid, 128, smem, s>>>(ma, mb, mc, M, N, K, alpha, beta,
                                                                (__nv_bfloat16 *)C, ldc, colmajor, ctma, ns);

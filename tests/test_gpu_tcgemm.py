@@ -18,7 +18,9 @@ def gpu():
 
 @pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 384, 256), (200, 130, 32), (1024, 96, 1024),
-                                   (300, 1000, 40), (1, 1, 16)])
+                                   (300, 1000, 40), (1, 1, 16),
+                                   # >= one tile per SM: the persistent warp-specialised kernel
+                                   (2048, 2048, 256), (2000, 2100, 96), (1536, 1536, 640), (4096, 1280, 64)])
 @pytest.mark.parametrize("beta", [0.0, 1.0])
 def test_tc_gemm_matches_fp32_reference(gpu, dt, M, N, K, beta):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
