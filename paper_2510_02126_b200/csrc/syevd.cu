@@ -613,11 +613,20 @@ dc_merge_prep_kernel(int p, const MergeInfo *__restrict__ mi, const double *__re
                      int *__restrict__ perm, double *__restrict__ Ds, double *__restrict__ zs,
                      double *__restrict__ DK, double *__restrict__ zK, int *__restrict__ Kpos,
                      int *__restrict__ Dpos, double *__restrict__ rot, int *__restrict__ counts,
-                     double *__restrict__ rho_out)
+                     double *__restrict__ rho_out, int use_smem)
 {
+    // the serial deflation scan runs on shared-memory copies when they fit (n <= nsmem):
+    // its chain of dependent loads/stores then costs shared- instead of global-memory latency
+    extern __shared__ double msm[];
     __shared__ double red[32];
+    __shared__ int s_cnt[3];
     const MergeInfo m = mi[blockIdx.x];
     const int lo = m.lo, mid = m.mid, hi = m.hi, n = hi - lo, n1 = mid - lo;
+    double *D = use_smem ? msm : Ds + lo;
+    double *z = use_smem ? msm + n : zs + lo;
+    double *R4 = use_smem ? msm + 2 * n : rot + 4 * lo;
+    int *Dp = use_smem ? reinterpret_cast<int *>(msm + 6 * n) : Dpos + lo;
+    int *Kp = use_smem ? Dp + n : Kpos + lo;
     const double rho_raw = e[mid - 1];
     const double sgn = (rho_raw < 0.0) ? -1.0 : 1.0;
     const double rho = 2.0 * fabs(rho_raw);
@@ -636,49 +645,57 @@ dc_merge_prep_kernel(int p, const MergeInfo *__restrict__ mi, const double *__re
             pos = (i - n1) + a;
         }
         perm[lo + pos] = i;
-        Ds[lo + pos] = val;
-        double z = (i < n1) ? Q[(long)(lo + i) * p + (mid - 1)] : sgn * Q[(long)(lo + i) * p + mid];
-        zs[lo + pos] = z * isq2;
+        D[pos] = val;
+        double zz = (i < n1) ? Q[(long)(lo + i) * p + (mid - 1)] : sgn * Q[(long)(lo + i) * p + mid];
+        z[pos] = zz * isq2;
     }
     __syncthreads();
     double mx = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) mx = fmax(mx, fmax(fabs(Ds[lo + i]), fabs(zs[lo + i])));
+    for (int i = threadIdx.x; i < n; i += blockDim.x) mx = fmax(mx, fmax(fabs(D[i]), fabs(z[i])));
     mx = block_max(mx, red);
     if (threadIdx.x == 0) {
         const double tol = 8.0 * 0x1p-52 * mx;
         int kk = 0, nd = 0, nr = 0, prev = -1;
         for (int k = 0; k < n; k++) {
-            if (rho * fabs(zs[lo + k]) <= tol) { Dpos[lo + nd++] = k; continue; }
+            if (rho * fabs(z[k]) <= tol) { Dp[nd++] = k; continue; }
             if (prev < 0) { prev = k; continue; }
-            double s = zs[lo + prev], c = zs[lo + k];
-            double tau = hypot(c, s);
-            double t = Ds[lo + k] - Ds[lo + prev];
-            c /= tau; s = -s / tau;
-            if (fabs(t * c * s) <= tol) {
-                zs[lo + k] = tau; zs[lo + prev] = 0.0;
-                rot[4 * (lo + nr) + 0] = prev; rot[4 * (lo + nr) + 1] = k;
-                rot[4 * (lo + nr) + 2] = c; rot[4 * (lo + nr) + 3] = s;
+            double sn = z[prev], c = z[k];
+            double tau = hypot(c, sn);
+            double t = D[k] - D[prev];
+            c /= tau; sn = -sn / tau;
+            if (fabs(t * c * sn) <= tol) {
+                z[k] = tau; z[prev] = 0.0;
+                R4[4 * nr + 0] = prev; R4[4 * nr + 1] = k;
+                R4[4 * nr + 2] = c; R4[4 * nr + 3] = sn;
                 nr++;
-                double tp = Ds[lo + prev] * c * c + Ds[lo + k] * s * s;
-                Ds[lo + k] = Ds[lo + prev] * s * s + Ds[lo + k] * c * c;
-                Ds[lo + prev] = tp;
-                Dpos[lo + nd++] = prev;
+                double tp = D[prev] * c * c + D[k] * sn * sn;
+                D[k] = D[prev] * sn * sn + D[k] * c * c;
+                D[prev] = tp;
+                Dp[nd++] = prev;
                 prev = k;
             } else {
-                Kpos[lo + kk++] = prev;
+                Kp[kk++] = prev;
                 prev = k;
             }
         }
-        if (prev >= 0) Kpos[lo + kk++] = prev;
+        if (prev >= 0) Kp[kk++] = prev;
         counts[2 * blockIdx.x] = kk;
         counts[2 * blockIdx.x + 1] = nr;
         rho_out[blockIdx.x] = rho;
+        s_cnt[0] = kk; s_cnt[1] = nd; s_cnt[2] = nr;
     }
     __syncthreads();
-    const int kk = counts[2 * blockIdx.x];
+    const int kk = s_cnt[0];
+    if (use_smem) {
+        const int nd = s_cnt[1], nr = s_cnt[2];
+        for (int i = threadIdx.x; i < n; i += blockDim.x) { Ds[lo + i] = D[i]; zs[lo + i] = z[i]; }
+        for (int i = threadIdx.x; i < nd; i += blockDim.x) Dpos[lo + i] = Dp[i];
+        for (int i = threadIdx.x; i < kk; i += blockDim.x) Kpos[lo + i] = Kp[i];
+        for (int i = threadIdx.x; i < 4 * nr; i += blockDim.x) rot[4 * lo + i] = R4[i];
+    }
     for (int i = threadIdx.x; i < kk; i += blockDim.x) {
-        DK[lo + i] = Ds[lo + Kpos[lo + i]];
-        zK[lo + i] = zs[lo + Kpos[lo + i]];
+        DK[lo + i] = D[Kp[i]];
+        zK[lo + i] = z[Kp[i]];
     }
 }
 
@@ -1133,8 +1150,19 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
             hm.push_back({hb[i], hb[i + width], hb[std::min(i + 2 * width, nl)]});
         const int nm = (int)hm.size();
         LYAP_CUDA_TRY(cudaMemcpyAsync(mi, hm.data(), sizeof(MergeInfo) * nm, cudaMemcpyHostToDevice, s));
-        dc_merge_prep_kernel<<<nm, 1024, 0, s>>>(p, mi, e, lam, W.Q, perm, Ds, zs, DK, zK, Kpos, Dpos, W.rot,
-                                                 counts, rho);
+        {
+            int maxn0 = 0;
+            for (auto &x : hm) maxn0 = std::max(maxn0, x.hi - x.lo);
+            const size_t msm = 56 * (size_t)maxn0;           // D, z, rot (4n), Dpos, Kpos
+            const int use = msm <= 200 * 1024 ? 1 : 0;
+            static bool attr_m = false;
+            if (!attr_m) {
+                cudaFuncSetAttribute(dc_merge_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                attr_m = true;
+            }
+            dc_merge_prep_kernel<<<nm, 1024, use ? msm : 0, s>>>(p, mi, e, lam, W.Q, perm, Ds, zs, DK, zK, Kpos, Dpos,
+                                                                 W.rot, counts, rho, use);
+        }
         LYAP_TRY(launched());
         int maxn = 0;
         for (auto &x : hm) maxn = std::max(maxn, x.hi - x.lo);
