@@ -250,15 +250,15 @@ __device__ __forceinline__ void row_load(Acc (&r)[BW], const Acc *src) {
     }
 }
 
-template <typename T, int BW, int RPT>
-__global__ void __launch_bounds__(512)
+template <typename T, int BW, int RPT, int NT>
+__global__ void __launch_bounds__(NT)
 gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T *__restrict__ X,
                          int *__restrict__ ipiv, int *__restrict__ moved, int *__restrict__ nmoved,
                          int *__restrict__ info, typename Prec<T>::acc *__restrict__ Tglob)
 {
     namespace cg = cooperative_groups;
     using Acc = typename Prec<T>::acc;
-    constexpr int NT = 512;
+    constexpr int NW = NT / 32;                                // warps per CTA
     cg::cluster_group cl = cg::this_cluster();
     const int q = (int)cl.block_rank(), NC = (int)cl.num_blocks();
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -267,8 +267,8 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
     constexpr int PW = 2 * BW + 4;                             // cand row, row j, |cand|, row index (16B-aligned rows)
     __shared__ __align__(16) Acc pub[2][PW];
     __shared__ __align__(16) Acc inbox[2][16][PW];             // pushed by every CTA of the cluster
-    __shared__ Acc redv[16];
-    __shared__ int redi[16];
+    __shared__ Acc redv[32];
+    __shared__ int redi[32];
     __shared__ int pivl[32];
     __shared__ int sflag;
     __shared__ Acc Ptop[32][33];
@@ -307,8 +307,8 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
         PPROF(0);
         __syncthreads();
         PPROF(1);
-        bv = lane < 16 ? redv[lane] : Acc(-1);
-        bi = lane < 16 ? redi[lane] : R;
+        bv = lane < NW ? redv[lane] : Acc(-1);
+        bi = lane < NW ? redi[lane] : R;
         warp_argmax<Acc>(bv, bi, lane);                        // every lane needs the CTA winner
         if (tid == 0) { pub[buf][2 * BW] = bv; pub[buf][2 * BW + 1] = Acc(bi); }
 #pragma unroll
@@ -323,8 +323,8 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
         __syncthreads();
         PPROF(2);
         // ---- push this CTA's candidate (and row j) into every CTA's inbox
-        if (wid < NC) {
-            Acc *dst = cl.map_shared_rank(&inbox[buf][q][0], wid);
+        for (int r = wid; r < NC; r += NW) {                   // warp r (mod NW) -> CTA r
+            Acc *dst = cl.map_shared_rank(&inbox[buf][q][0], r);
             for (int e = lane; e < PW; e += 32) dst[e] = pub[buf][e];
         }
         cl.sync();
@@ -427,17 +427,20 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
             }
         }
         __syncthreads();
-        Acc tval[2] = {Acc(0), Acc(0)};                        // 512 threads: rows ti and ti + 16
+        constexpr int RT = (32 + NW - 1) / NW;                   // rows of T per thread
+        Acc tval[RT];
+#pragma unroll
+        for (int hh = 0; hh < RT; hh++) tval[hh] = Acc(0);
         const int ti = tid / 32, tc = tid % 32;
 #pragma unroll
-        for (int hh = 0; hh < 2; hh++)
-            if (ti + 16 * hh < b && tc < b)
+        for (int hh = 0; hh < RT; hh++)
+            if (ti + NW * hh < b && tc < b)
 #pragma unroll
                 for (int t = 0; t < BW; t++)
-                    if (t < b) tval[hh] = fma(Uw[(ti + 16 * hh) * 32 + t], Lw[t * 32 + tc], tval[hh]);
+                    if (t < b) tval[hh] = fma(Uw[(ti + NW * hh) * 32 + t], Lw[t * 32 + tc], tval[hh]);
         __syncthreads();
-        for (int hh = 0; hh < 2; hh++)
-            if (ti + 16 * hh < b && tc < b) Tw[(ti + 16 * hh) * 32 + tc] = tval[hh];
+        for (int hh = 0; hh < RT; hh++)
+            if (ti + NW * hh < b && tc < b) Tw[(ti + NW * hh) * 32 + tc] = tval[hh];
     }
     cl.sync();
     if (q != 0) {
@@ -725,11 +728,14 @@ static int gje_panel_launch(cudaStream_t s, int n, int k, int b, T *A, GjeWork &
     using Acc = typename Prec<T>::acc;
     constexpr int BW = std::is_same<T, double>::value ? 16 : 32;
     const int R = n - k;
-    int nc = std::max(1, std::min(16, ceil_div(R, 512)));
+    // NTh threads per CTA, one panel row per thread (two when the cluster is full): 512 is
+    // measured faster up to ~8K panel rows, 1024 (fewer CTAs in the cluster) above
+    const int NTh = (R > 8192 && !env_flag("LYAP_GJE_512")) ? 1024 : 512;
+    int nc = std::max(1, std::min(16, ceil_div(R, NTh)));
     if (const char *e = getenv("LYAP_GJE_NC")) nc = std::max(1, std::min(16, atoi(e)));
     const int RB = std::max(b, ceil_div(R, nc));
     nc = ceil_div(R, RB);
-    if (RB > 2 * 512 || b > BW || env_flag("LYAP_GJE_1CTA")) {
+    if (RB > 2 * NTh || b > BW || env_flag("LYAP_GJE_1CTA")) {
         bool use_smem;
         size_t sm = gje_panel_smem(n, Prec<T>::code, b, R, &use_smem);
         static bool attr1 = false;
@@ -741,16 +747,20 @@ static int gje_panel_launch(cudaStream_t s, int n, int k, int b, T *A, GjeWork &
                                                 (Acc *)w.Pglob, use_smem ? 1 : 0);
         return launched();
     }
-    auto kern = (RB > 512) ? gje_panel_cluster_kernel<T, BW, 2> : gje_panel_cluster_kernel<T, BW, 1>;
+    void (*kern)(int, int, int, int, const T *, T *, int *, int *, int *, int *, Acc *);
+    if (NTh == 1024) kern = (RB > 1024) ? gje_panel_cluster_kernel<T, BW, 2, 1024> : gje_panel_cluster_kernel<T, BW, 1, 1024>;
+    else kern = (RB > 512) ? gje_panel_cluster_kernel<T, BW, 2, 512> : gje_panel_cluster_kernel<T, BW, 1, 512>;
     static bool attr = false;
     if (!attr) {
-        LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 1, 1024>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 2, 1024>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 1, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 2, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nc, 1, 1);
-    cfg.blockDim = dim3(512, 1, 1);
+    cfg.blockDim = dim3(NTh, 1, 1);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
