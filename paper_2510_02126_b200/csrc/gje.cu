@@ -574,6 +574,29 @@ __global__ void gje_outer_perm_kernel(int K0, int nb, const int *__restrict__ ip
     }
 }
 
+// (1') O(n) parallel alternative to the warp replay: with invprev = the inverse of rowperm
+// before the block and rowperm after it, position i (>= K0) now holds the row that was at
+// src = invprev[rowperm[i]].  The (dst, src) list order is irrelevant (each dst once);
+// slot_of[y] = list index of pivot row K0 + y (or -1), for the scatter.
+__global__ void gje_inv_snapshot_kernel(int n, const int *__restrict__ rowperm, int *__restrict__ invprev)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) invprev[rowperm[i]] = i;
+}
+__global__ void gje_outer_perm2_kernel(int n, int K0, int nb, const int *__restrict__ rowperm,
+                                       const int *__restrict__ invprev, int *__restrict__ omoved,
+                                       int *__restrict__ onmoved, int *__restrict__ slot_of)
+{
+    for (int i = K0 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int src = invprev[rowperm[i]];
+        if (src != i) {
+            const int t = atomicAdd(onmoved, 1);
+            omoved[2 * t] = i;
+            omoved[2 * t + 1] = src;
+            if (i < K0 + nb) slot_of[i - K0] = t;
+        }
+    }
+}
+
 // (2) gather the moved source rows' rest entries
 template <typename T>
 __global__ void gje_outer_gather_kernel(int n, int K0, int nb, const T *__restrict__ A, const int *__restrict__ omoved,
@@ -593,7 +616,8 @@ __global__ void gje_outer_gather_kernel(int n, int K0, int nb, const T *__restri
 template <typename T>
 __global__ void __launch_bounds__(256)
 gje_outer_scatter_kernel(int n, int K0, int nb, T *__restrict__ A, const int *__restrict__ omoved,
-                         const int *__restrict__ onmoved, const T *__restrict__ tmp2, T *__restrict__ Bo)
+                         const int *__restrict__ onmoved, const T *__restrict__ tmp2, T *__restrict__ Bo,
+                         const int *__restrict__ slot_of)
 {
     const int m = *onmoved;
     const int nrest = n - nb;
@@ -601,11 +625,7 @@ gje_outer_scatter_kernel(int n, int K0, int nb, T *__restrict__ A, const int *__
         // pivot rows: tile of 32 rest columns x nb rows
         __shared__ T tile[32][33];
         __shared__ int slot[GJE_NB];
-        for (int y = threadIdx.x; y < nb; y += blockDim.x) {
-            int sl = -1;
-            for (int t = 0; t < m; t++) if (omoved[2 * t] == K0 + y) { sl = t; break; }
-            slot[y] = sl;
-        }
+        for (int y = threadIdx.x; y < nb; y += blockDim.x) slot[y] = slot_of[y];
         __syncthreads();
         const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;     // 32 x 8
         for (int e0 = blockIdx.x * 32; e0 < nrest; e0 += gridDim.x * 32) {
@@ -684,8 +704,8 @@ int GjeWork::alloc(int n_, int prec_) {
     if ((prec == LYAP_FP16 || prec == LYAP_BF16) && n % 8 == 0 && n >= 2 * GJE_NB) {
         LYAP_CUDA_TRY(cudaMalloc(&Bo, es * (size_t)n * GJE_NB));
         LYAP_CUDA_TRY(cudaMalloc(&tmp2, es * (size_t)n * 2 * GJE_NB));
-        LYAP_CUDA_TRY(cudaMalloc(&oints, sizeof(int) * (4 * GJE_NB + 4)));
-        omoved = oints; onmoved = oints + 4 * GJE_NB;
+        LYAP_CUDA_TRY(cudaMalloc(&oints, sizeof(int) * (5 * GJE_NB + 8 + (size_t)n)));
+        omoved = oints; onmoved = oints + 4 * GJE_NB; slot_of = onmoved + 4; invprev = slot_of + GJE_NB;
     }
     LYAP_CUDA_TRY(cudaMalloc(&ints, sizeof(int) * (size_t)(4 * n + 4 * b + 8)));
     ipiv = ints; rowperm = ipiv + n; invperm = rowperm + n; moved = invperm + n;
@@ -696,7 +716,8 @@ int GjeWork::alloc(int n_, int prec_) {
 void GjeWork::release() {
     cudaFree(X); cudaFree(B); cudaFree(tmp); cudaFree(Pglob); cudaFree(Tg); cudaFree(Bo); cudaFree(tmp2);
     cudaFree(ints); cudaFree(oints);
-    X = B = tmp = nullptr; Pglob = Tg = Bo = tmp2 = nullptr; ints = oints = omoved = onmoved = nullptr;
+    X = B = tmp = nullptr; Pglob = Tg = Bo = tmp2 = nullptr;
+    ints = oints = omoved = onmoved = slot_of = invprev = nullptr;
 }
 
 // X rows above the panel: X[i, :] = -A[i, k:k+b] T for i < k.  One warp per row: the
@@ -796,6 +817,10 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
     const int NBo = two_level ? GJE_NB : n;
     for (int K0 = 0; K0 < n; K0 += NBo) {
         const int nbk = std::min(NBo, n - K0);
+        if (two_level && n - nbk > 0) {
+            gje_inv_snapshot_kernel<<<std::min(ceil_div(n, 256), 592), 256, 0, s>>>(n, w.rowperm, w.invprev);
+            LYAP_TRY(launched());
+        }
         const int c0 = two_level ? K0 : 0, c1 = two_level ? K0 + nbk : n;
         for (int k = K0; k < K0 + nbk; k += b0) {
             const int b = std::min(b0, K0 + nbk - k);
@@ -823,14 +848,17 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
             }
         }
         if (two_level && n - nbk > 0) {
-            gje_outer_perm_kernel<<<1, 32, 0, s>>>(K0, nbk, w.ipiv, w.omoved, w.onmoved);
+            LYAP_CUDA_TRY(cudaMemsetAsync(w.onmoved, 0, sizeof(int), s));
+            LYAP_CUDA_TRY(cudaMemsetAsync(w.slot_of, 0xFF, sizeof(int) * GJE_NB, s));
+            gje_outer_perm2_kernel<<<std::min(ceil_div(n - K0, 256), 592), 256, 0, s>>>(n, K0, nbk, w.rowperm, w.invprev,
+                                                                                      w.omoved, w.onmoved, w.slot_of);
             LYAP_TRY(launched());
             const int gx = std::min(ceil_div(n - nbk, 256), 64);
             gje_outer_gather_kernel<T><<<dim3(gx, 2 * nbk), 256, 0, s>>>(n, K0, nbk, A, w.omoved, w.onmoved,
                                                                        (T *)w.tmp2);
             LYAP_TRY(launched());
             gje_outer_scatter_kernel<T><<<dim3(std::min(ceil_div(n - nbk, 32), 592), 1 + 2 * nbk), 256, 0, s>>>(
-                n, K0, nbk, A, w.omoved, w.onmoved, (const T *)w.tmp2, (T *)w.Bo);
+                n, K0, nbk, A, w.omoved, w.onmoved, (const T *)w.tmp2, (T *)w.Bo, w.slot_of);
             LYAP_TRY(launched());
             KTimer kt(KC_GJE_UPDATE, s);
             // A[:, rest] += X_outer B_outer, X_outer = the block columns (ld n)

@@ -10,7 +10,7 @@ constexpr int GJE_NB = 256;       // outer block of the two-level Gauss-Jordan s
 struct GjeWork {
     int n = 0, prec = 0;
     void *X = nullptr, *B = nullptr, *tmp = nullptr, *Pglob = nullptr, *Tg = nullptr, *Bo = nullptr, *tmp2 = nullptr;
-    int *oints = nullptr, *omoved = nullptr, *onmoved = nullptr;
+    int *oints = nullptr, *omoved = nullptr, *onmoved = nullptr, *slot_of = nullptr, *invprev = nullptr;
     int *ints = nullptr;
     int *ipiv = nullptr, *rowperm = nullptr, *invperm = nullptr, *moved = nullptr;
     int *nmoved = nullptr, *info = nullptr, *tmp_perm = nullptr;
