@@ -472,7 +472,7 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
 
 // gather moved source rows (full width) and their rowperm entries into tmp
 template <typename T>
-__global__ void gje_gather_kernel(int n, int k, const T *__restrict__ A, const int *__restrict__ moved,
+__global__ void gje_gather_kernel(int n, int k, int c0, int c1, const T *__restrict__ A, const int *__restrict__ moved,
                                   const int *__restrict__ nmoved, T *__restrict__ tmp,
                                   const int *__restrict__ rowperm, int *__restrict__ tmp_perm)
 {
@@ -480,7 +480,7 @@ __global__ void gje_gather_kernel(int n, int k, const T *__restrict__ A, const i
     int t = blockIdx.y;
     if (t >= m) return;
     int src = k + moved[2 * t + 1];
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+    for (int c = c0 + blockIdx.x * blockDim.x + threadIdx.x; c < c1; c += gridDim.x * blockDim.x)
         tmp[(long)t * n + c] = A[(long)src * n + c];
     if (blockIdx.x == 0 && threadIdx.x == 0) tmp_perm[t] = rowperm[src];
 }
@@ -705,6 +705,11 @@ int GjeWork::alloc(int n_, int prec_) {
         LYAP_CUDA_TRY(cudaMalloc(&Bo, es * (size_t)n * GJE_NB));
         LYAP_CUDA_TRY(cudaMalloc(&tmp2, es * (size_t)n * 2 * GJE_NB));
         LYAP_CUDA_TRY(cudaMalloc(&oints, sizeof(int) * (5 * GJE_NB + 8 + (size_t)n)));
+        int lo_p = 0, hi_p = 0;
+        cudaDeviceGetStreamPriorityRange(&lo_p, &hi_p);
+        LYAP_CUDA_TRY(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi_p));
+        LYAP_CUDA_TRY(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
+        LYAP_CUDA_TRY(cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming));
         omoved = oints; onmoved = oints + 4 * GJE_NB; slot_of = onmoved + 4; invprev = slot_of + GJE_NB;
     }
     LYAP_CUDA_TRY(cudaMalloc(&ints, sizeof(int) * (size_t)(4 * n + 4 * b + 8)));
@@ -716,6 +721,9 @@ int GjeWork::alloc(int n_, int prec_) {
 void GjeWork::release() {
     cudaFree(X); cudaFree(B); cudaFree(tmp); cudaFree(Pglob); cudaFree(Tg); cudaFree(Bo); cudaFree(tmp2);
     cudaFree(ints); cudaFree(oints);
+    if (side) { cudaStreamSynchronize(side); cudaStreamDestroy(side); side = nullptr; }
+    if (ev_a) { cudaEventDestroy(ev_a); ev_a = nullptr; }
+    if (ev_b) { cudaEventDestroy(ev_b); ev_b = nullptr; }
     X = B = tmp = nullptr; Pglob = Tg = Bo = tmp2 = nullptr;
     ints = oints = omoved = onmoved = slot_of = invprev = nullptr;
 }
@@ -815,10 +823,19 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
     const bool two_level = half_t && !use_simt_gemm() && n % 8 == 0 && n >= 2 * GJE_NB && w.Bo != nullptr &&
                            !env_flag("LYAP_GJE_1LEVEL");
     const int NBo = two_level ? GJE_NB : n;
+    // look-ahead (two-level only): the inner steps (pivot panels) of block K0+NB run on the
+    // high-priority side stream P while the main stream finishes the outer update of block
+    // K0; the next block's columns are updated first so P can start early.
+    const bool ahead = two_level && w.side != nullptr && !env_flag("LYAP_GJE_NO_LOOKAHEAD");
+    cudaStream_t P = ahead ? w.side : s;
+    if (ahead) {
+        LYAP_CUDA_TRY(cudaEventRecord(w.ev_a, s));
+        LYAP_CUDA_TRY(cudaStreamWaitEvent(P, w.ev_a, 0));
+    }
     for (int K0 = 0; K0 < n; K0 += NBo) {
         const int nbk = std::min(NBo, n - K0);
         if (two_level && n - nbk > 0) {
-            gje_inv_snapshot_kernel<<<std::min(ceil_div(n, 256), 592), 256, 0, s>>>(n, w.rowperm, w.invprev);
+            gje_inv_snapshot_kernel<<<std::min(ceil_div(n, 256), 592), 256, 0, P>>>(n, w.rowperm, w.invprev);
             LYAP_TRY(launched());
         }
         const int c0 = two_level ? K0 : 0, c1 = two_level ? K0 + nbk : n;
@@ -826,26 +843,31 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
             const int b = std::min(b0, K0 + nbk - k);
             {
                 // algorithmic work: panel LU ~ (n-k) b^2 flops + multiplier block X 2 n b^2
-                KTimer kt(KC_GJE_PANEL, s, (double)(n - k) * b * b + 2.0 * n * b * b,
+                KTimer kt(KC_GJE_PANEL, P, (double)(n - k) * b * b + 2.0 * n * b * b,
                           (double)sizeof(T) * ((double)(n - k) * b + (double)n * b));
-                LYAP_TRY(gje_panel_launch<T>(s, n, k, b, A, w));
+                LYAP_TRY(gje_panel_launch<T>(P, n, k, b, A, w));
             }
             LYAP_TRY(launched());
             dim3 gg(ceil_div(c1 - c0, 256) < 8 ? ceil_div(c1 - c0, 256) : 8, 2 * b);
-            gje_gather_kernel<T><<<gg, 256, 0, s>>>(n, k, A, w.moved, w.nmoved, (T *)w.tmp, w.rowperm, w.tmp_perm);
+            gje_gather_kernel<T><<<gg, 256, 0, P>>>(n, k, c0, c1, A, w.moved, w.nmoved, (T *)w.tmp, w.rowperm,
+                                                    w.tmp_perm);
             LYAP_TRY(launched());
             dim3 gp(std::min(ceil_div(c1 - c0, 256), 8), 3 * b + std::min(ceil_div((long)n * b, 8 * 256), 512));
-            gje_prep_kernel<T><<<gp, 256, 0, s>>>(n, k, b, c0, c1, A, w.moved, w.nmoved, (const T *)w.tmp,
+            gje_prep_kernel<T><<<gp, 256, 0, P>>>(n, k, b, c0, c1, A, w.moved, w.nmoved, (const T *)w.tmp,
                                                   w.tmp_perm, w.rowperm, (T *)w.B);
             LYAP_TRY(launched());
             {
-                KTimer kt(KC_GJE_UPDATE, s);
+                KTimer kt(KC_GJE_UPDATE, P);
                 if (two_level)
-                    LYAP_TRY(tc_gemm(s, Prec<T>::code, n, nbk, b, 1.0f, w.X, b, (const T *)w.B + (size_t)K0 * b, b,
+                    LYAP_TRY(tc_gemm(P, Prec<T>::code, n, nbk, b, 1.0f, w.X, b, (const T *)w.B + (size_t)K0 * b, b,
                                      1.0f, A + K0, n, 0));
                 else
-                    LYAP_TRY(gemm_update(s, n, b, (const T *)w.X, (const T *)w.B, A));
+                    LYAP_TRY(gemm_update(P, n, b, (const T *)w.X, (const T *)w.B, A));
             }
+        }
+        if (ahead) {
+            LYAP_CUDA_TRY(cudaEventRecord(w.ev_b, P));             // inner steps of this block done
+            LYAP_CUDA_TRY(cudaStreamWaitEvent(s, w.ev_b, 0));
         }
         if (two_level && n - nbk > 0) {
             LYAP_CUDA_TRY(cudaMemsetAsync(w.onmoved, 0, sizeof(int), s));
@@ -861,13 +883,24 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
                 n, K0, nbk, A, w.omoved, w.onmoved, (const T *)w.tmp2, (T *)w.Bo, w.slot_of);
             LYAP_TRY(launched());
             KTimer kt(KC_GJE_UPDATE, s);
-            // A[:, rest] += X_outer B_outer, X_outer = the block columns (ld n)
-            if (K0 > 0)
-                LYAP_TRY(tc_gemm(s, Prec<T>::code, n, K0, nbk, 1.0f, A + K0, n, (const T *)w.Bo, nbk, 1.0f, A, n, 0));
+            // A[:, rest] += X_outer B_outer, X_outer = the block columns (ld n); the next
+            // block's columns first, then (look-ahead) the side stream may start on them
             const int cr = K0 + nbk;
-            if (cr < n)
-                LYAP_TRY(tc_gemm(s, Prec<T>::code, n, n - cr, nbk, 1.0f, A + K0, n, (const T *)w.Bo + (size_t)cr * nbk,
+            const int cn = ahead ? std::min(n, cr + NBo) : cr;
+            if (ahead && cn > cr) {
+                LYAP_TRY(tc_gemm(s, Prec<T>::code, n, cn - cr, nbk, 1.0f, A + K0, n, (const T *)w.Bo + (size_t)cr * nbk,
                                  nbk, 1.0f, A + cr, n, 0));
+                LYAP_CUDA_TRY(cudaEventRecord(w.ev_a, s));
+                LYAP_CUDA_TRY(cudaStreamWaitEvent(P, w.ev_a, 0));
+            }
+            // with look-ahead, leave SMs for the pivot-panel cluster running concurrently on P
+            const int cap = ahead ? 148 - 16 : 0;
+            if (K0 > 0)
+                LYAP_TRY(tc_gemm(s, Prec<T>::code, n, K0, nbk, 1.0f, A + K0, n, (const T *)w.Bo, nbk, 1.0f, A, n, 0,
+                                 cap));
+            if (cn < n)
+                LYAP_TRY(tc_gemm(s, Prec<T>::code, n, n - cn, nbk, 1.0f, A + K0, n, (const T *)w.Bo + (size_t)cn * nbk,
+                                 nbk, 1.0f, A + cn, n, 0, cap));
         }
     }
     invperm_kernel<<<ceil_div(n, 256), 256, 0, s>>>(n, w.rowperm, w.invperm);

@@ -11,6 +11,8 @@ struct GjeWork {
     int n = 0, prec = 0;
     void *X = nullptr, *B = nullptr, *tmp = nullptr, *Pglob = nullptr, *Tg = nullptr, *Bo = nullptr, *tmp2 = nullptr;
     int *oints = nullptr, *omoved = nullptr, *onmoved = nullptr, *slot_of = nullptr, *invprev = nullptr;
+    cudaStream_t side = nullptr;          // look-ahead stream of the two-level scheme
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
     int *ints = nullptr;
     int *ipiv = nullptr, *rowperm = nullptr, *invperm = nullptr, *moved = nullptr;
     int *nmoved = nullptr, *info = nullptr, *tmp_perm = nullptr;
@@ -26,8 +28,9 @@ inline bool use_simt_gemm() {
     return v == 1;
 }
 // tcgen05 GEMM (tc_gemm.cu): C = alpha A B^T + beta C, 16-bit A (M x K), B (N x K) row-major
+// max_ctas > 0 caps the persistent kernel's grid (SMs left free for concurrent work)
 int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const void *A, long lda, const void *B,
-            long ldb, float beta, void *C, long ldc, int colmajor);
+            long ldb, float beta, void *C, long ldc, int colmajor, int max_ctas = 0);
 int col_gather(cudaStream_t s, int n, int prec, const void *G, const int *invperm, void *out);
 template <typename T> int gemm_update(cudaStream_t s, int n, int b, const T *X, const T *B, T *A);
 

@@ -444,7 +444,7 @@ int make_map(CUtensorMap *m, const void *ptr, int prec, long rows, long cols, lo
 
 // C = alpha * A (M x K, ld lda) * B^T (B: N x K, ld ldb) + beta * C  (C ld ldc, row- or column-major)
 int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const void *A, long lda, const void *B,
-            long ldb, float beta, void *C, long ldc, int colmajor)
+            long ldb, float beta, void *C, long ldc, int colmajor, int max_ctas)
 {
     if (M <= 0 || N <= 0 || K <= 0) return LYAP_OK;
     if (prec != LYAP_BF16 && prec != LYAP_FP16) return LYAP_ERR_ARG;
@@ -477,7 +477,7 @@ int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const vo
     }
     const int tiles = (int)(grid.x * grid.y);
     if (ctma && tiles >= nsm && !env_flag("LYAP_TC_NONPERSISTENT")) {
-        const int g = std::min(tiles, nsm);
+        const int g = std::min(tiles, max_ctas > 0 ? std::min(max_ctas, nsm) : nsm);
         if (prec == LYAP_BF16)
             tc_gemm_persistent_kernel<__nv_bfloat16><<<g, tc::PTHREADS, tc::PSMEM, s>>>(ma, mb, mc, M, N, K, alpha, beta);
         else

@@ -1,0 +1,24 @@
+"""Device time of the fp16 sign-Newton A-sequence (preallocated solver handle) at order n."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2510_02126_b200 as G
+for n in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "4096").split(",")]:
+    g = torch.Generator(device="cuda").manual_seed(n)
+    Q, _ = torch.linalg.qr(torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g))
+    lam = torch.logspace(0, 2, n, dtype=torch.float64, device="cuda")
+    A = -(Q * lam[None, :]) @ Q.T
+    s = G.Solver(n, us="fp16", max_cols=64)
+    out = s.newton_aseq(A)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(2):
+        out = s.newton_aseq(A)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 2
+    k = out["steps"]
+    print(f"n={n}: A-sequence {ms:8.2f} ms, {k} inversions, {ms / k:7.2f} ms/inversion, "
+          f"{k * 2 * n ** 3 / (ms / 1e3) / 1e12:7.2f} TFLOP/s", flush=True)
+    del s, A, Q
+    torch.cuda.empty_cache()
