@@ -63,6 +63,7 @@ struct lyap_ir_ctx {
     cudaEvent_t ev[8];
     double t_newton = 0, t_res = 0, t_upd = 0;
     bool zorth = false;        // leading factor columns are orthonormal (set by the IR loop)
+    bool y_diag = false;       // the Newton inner factor Y_k is diagonal (zside)
 };
 
 namespace {
@@ -176,7 +177,10 @@ int trunc_ldlt(lyap_ir_ctx *h, int c, int *cnew) {
     const int k = std::min(n, c);
     LYAP_TRY(nk_to_f64(s, h->us, (long)n * c, h->Zt, h->Zd, 1.0));
     LYAP_TRY(qr_f64(s, n, c, h->Zd, h->U, h->Tm, h->qr));
-    LYAP_TRY(dgemm_cm(s, false, false, k, c, c, 1.0, h->Tm, k, h->Yc, h->PZ, 0.0, h->TN, k));
+    // T Y T^T; Y is diagonal whenever the inner factor was (every correction equation and
+    // any diagonal user S): then T Y is a column scaling (bitwise the same products)
+    if (h->y_diag) LYAP_TRY(nk_scale_cols(s, k, c, h->Tm, k, h->Yc, h->PZ, h->TN, k));
+    else LYAP_TRY(dgemm_cm(s, false, false, k, c, c, 1.0, h->Tm, k, h->Yc, h->PZ, 0.0, h->TN, k));
     LYAP_TRY(dgemm_cm(s, false, true, k, k, c, 1.0, h->TN, k, h->Tm, k, 0.0, h->Hm, k));
     LYAP_TRY(syev_f64(s, k, h->Hm, h->wv, h->Vm, h->eig));
     LYAP_TRY(nk_select(s, k, h->wv, unit_roundoff(h->us), 1, h->ibuf, h->ibuf + 3 * h->PW));
@@ -201,12 +205,25 @@ int trunc_chol(lyap_ir_ctx *h, int c, int *cnew) {
     return LYAP_OK;
 }
 
+// is the m x m device matrix S diagonal? (read back; m is the small inner dimension)
+int is_diag_dev(lyap_ir_ctx *h, const double *S, int m, bool *out) {
+    std::vector<double> hs((size_t)m * m);
+    LYAP_TRY(sync_read(h, hs.data(), S, sizeof(double) * hs.size()));
+    bool d = true;
+    for (int j = 0; j < m && d; j++)
+        for (int i = 0; i < m; i++)
+            if (i != j && hs[i + (size_t)j * m] != 0.0) { d = false; break; }
+    *out = d;
+    return LYAP_OK;
+}
+
 // ------------------------------------------------------------------ Z side
 // Algorithm 4 (ldlt) / Algorithm 3 on the cached A-sequence.  Output fp64
 // Zout (n x c, ld n) and, for LDL^T, Yout (c x c, ld ldy).
 int zside(lyap_ir_ctx *h, bool ldlt, const double *L, int m, const double *S, double *Zout, double *Yout,
-          int ldy, int *cout) {
+          int ldy, int *cout, bool s_diag) {
     const int n = h->n, us = h->us;
+    h->y_diag = ldlt && s_diag;             // Y_k stays diagonal through blkdiag scaling and truncation
     cudaStream_t s = h->s;
     if (m > h->PZ / 2) return LYAP_ERR_CAPACITY;
     LYAP_TRY(nk_load_factor(s, us, (long)n * m, L, h->Zt, h->scal, SC_EL));
@@ -317,9 +334,26 @@ int res_fac(lyap_ir_ctx *h, const double *A, const double *L, int m, const doubl
     const int k = std::min(n, p);
     LYAP_TRY(build_F(h, A, L, m, c, Z));
     LYAP_TRY(thin_qr_F(h, p, c));
-    LYAP_TRY(nk_build_N(s, c, m, Y, ldy, Y ? S : nullptr, h->Nm));
-    LYAP_TRY(dgemm_cm(s, false, false, k, p, p, 1.0, h->Tm, k, h->Nm, p, 0.0, h->TN, k));
-    LYAP_TRY(dgemm_cm(s, false, true, k, k, p, 1.0, h->TN, k, h->Tm, k, 0.0, h->Hm, k));
+    // H = T N T^T with N = [[0, Y, 0], [Y, 0, 0], [0, 0, S]] (Y = I for Cholesky, S = I
+    // if absent): H = G + G^T + T3 S T3^T, G = T1 Y T2^T with T = [T1 T2 T3] -- the
+    // structure of N saves two thirds of the dense T N T^T products
+    {
+        const double *T1 = h->Tm, *T2 = h->Tm + (size_t)k * c, *T3 = h->Tm + (size_t)2 * k * c;
+        const double *W = T1;
+        if (Y) {
+            LYAP_TRY(dgemm_cm(s, false, false, k, c, c, 1.0, T1, k, Y, ldy, 0.0, h->TN, k));
+            W = h->TN;
+        }
+        LYAP_TRY(dgemm_cm(s, false, true, k, k, c, 1.0, W, k, T2, k, 0.0, h->Hm, k));
+        LYAP_TRY(nk_sym_add(s, k, h->Hm, k));
+        const double *W3 = T3;
+        if (Y && S) {
+            double *w3 = h->TN + (size_t)k * c;
+            LYAP_TRY(dgemm_cm(s, false, false, k, m, m, 1.0, T3, k, S, m, 0.0, w3, k));
+            W3 = w3;
+        }
+        LYAP_TRY(dgemm_cm(s, false, true, k, k, m, 1.0, W3, k, T3, k, 1.0, h->Hm, k));
+    }
     LYAP_TRY(syev_f64(s, k, h->Hm, h->wv, h->Vm, h->eig));
     LYAP_TRY(nk_sumsq(s, k, h->wv, h->scal + SC_TR));
     int *cnt = h->ibuf + 3 * h->PW;
@@ -422,7 +456,9 @@ int ir_solve(lyap_ir_ctx *h, const double *A, const double *L, int m, const doub
         *rank_out = 0;
         return (rc == LYAP_ERR_CUDA) ? rc : LYAP_OK;
     }
-    LYAP_TRY(zside(h, ldlt, L, m, S, h->Zsol[cur], h->Ysol[cur], h->PW, &c));
+    bool s_diag = false;
+    if (ldlt) LYAP_TRY(is_diag_dev(h, S, m, &s_diag));
+    LYAP_TRY(zside(h, ldlt, L, m, S, h->Zsol[cur], h->Ysol[cur], h->PW, &c, s_diag));
     R.newton_calls = 1;
     LYAP_CUDA_TRY(cudaEventRecord(h->ev[1], s));
     LYAP_CUDA_TRY(cudaEventSynchronize(h->ev[1]));
@@ -479,10 +515,10 @@ int ir_solve(lyap_ir_ctx *h, const double *A, const double *L, int m, const doub
         }
         int cd = 0, cm = 0;
         if (ldlt) {
-            LYAP_TRY(zside(h, true, h->Ld, r, h->Sd, h->Zdel, h->Ydel, h->PZ, &cd));
+            LYAP_TRY(zside(h, true, h->Ld, r, h->Sd, h->Zdel, h->Ydel, h->PZ, &cd, true));   // Sd diagonal
         } else {
-            if (r > 0) LYAP_TRY(zside(h, false, h->Ld, r, nullptr, h->Zdel, nullptr, 0, &cd));
-            if (rmm > 0) LYAP_TRY(zside(h, false, h->Lm, rmm, nullptr, h->Zdel2, nullptr, 0, &cm));
+            if (r > 0) LYAP_TRY(zside(h, false, h->Ld, r, nullptr, h->Zdel, nullptr, 0, &cd, false));
+            if (rmm > 0) LYAP_TRY(zside(h, false, h->Lm, rmm, nullptr, h->Zdel2, nullptr, 0, &cm, false));
         }
         R.newton_calls++;
         LYAP_CUDA_TRY(cudaEventRecord(h->ev[5], s));
@@ -658,7 +694,9 @@ int lyap_newton_get_inverse(lyap_ir_handle h, int j, void *out) {
 
 int lyap_newton_z(lyap_ir_handle h, int ldlt, const double *L, int m, const double *S, double *Z, double *Y, int *c) {
     if (!h || !L || !Z || !c || (ldlt && (!S || !Y))) return LYAP_ERR_ARG;
-    int rc = zside(h, ldlt != 0, L, m, S, Z, Y, h->cmax, c);
+    bool s_diag = false;
+    if (ldlt) LYAP_TRY(is_diag_dev(h, S, m, &s_diag));
+    int rc = zside(h, ldlt != 0, L, m, S, Z, Y, h->cmax, c, s_diag);
     if (rc == LYAP_OK) LYAP_CUDA_TRY(cudaStreamSynchronize(h->s));
     return rc;
 }

@@ -513,6 +513,39 @@ int nk_zero(cudaStream_t s, long len, double *x)
     zero_kernel<<<grid_for(len), 256, 0, s>>>(len, x);
     return launched();
 }
+// H <- H + H^T in place (k x k, ld ldh): each unordered pair {i, j} by the thread of (i <= j)
+__global__ void sym_add_kernel(int k, double *__restrict__ H, int ldh)
+{
+    const long tot = (long)k * k;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(e % k), j = (int)(e / k);
+        if (i > j) continue;
+        const double v = H[i + (long)j * ldh] + H[j + (long)i * ldh];
+        H[i + (long)j * ldh] = v;
+        H[j + (long)i * ldh] = v;
+    }
+}
+// out[:, j] = T[:, j] * D[j][j]  (k x c; D with leading dimension ldd)
+__global__ void scale_cols_kernel(int k, int c, const double *__restrict__ T, int ldt, const double *__restrict__ D,
+                                  int ldd, double *__restrict__ out, int ldo)
+{
+    const long tot = (long)k * c;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+        const int i = (int)(e % k), j = (int)(e / k);
+        out[i + (long)j * ldo] = T[i + (long)j * ldt] * D[j + (long)j * ldd];
+    }
+}
+int nk_sym_add(cudaStream_t s, int k, double *H, int ldh)
+{
+    sym_add_kernel<<<grid_for((long)k * k), 256, 0, s>>>(k, H, ldh);
+    return launched();
+}
+int nk_scale_cols(cudaStream_t s, int k, int c, const double *T, int ldt, const double *D, int ldd, double *out, int ldo)
+{
+    scale_cols_kernel<<<grid_for((long)k * c), 256, 0, s>>>(k, c, T, ldt, D, ldd, out, ldo);
+    return launched();
+}
+
 int nk_build_N(cudaStream_t s, int c, int m, const double *Y, int ldy, const double *S, double *N)
 {
     long p = 2L * c + m;

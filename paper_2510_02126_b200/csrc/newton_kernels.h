@@ -42,6 +42,8 @@ int nk_round(cudaStream_t s, long len, double *x, int prec);
 int nk_copy_block(cudaStream_t s, int rows, int cols, const double *a, int lda, double *b, int ldb, double f);
 int nk_zero(cudaStream_t s, long len, double *x);
 int nk_build_N(cudaStream_t s, int c, int m, const double *Y, int ldy, const double *S, double *N);
+int nk_sym_add(cudaStream_t s, int k, double *H, int ldh);
+int nk_scale_cols(cudaStream_t s, int k, int c, const double *T, int ldt, const double *D, int ldd, double *out, int ldo);
 int nk_build_blkdiag(cudaStream_t s, int c, int cd, const double *Y, int ldy, const double *Yd, int ldyd, int cp,
                      double *U);
 int nk_trace_prod(cudaStream_t s, int k, const double *P, double *out);
