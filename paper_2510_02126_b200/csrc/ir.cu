@@ -64,6 +64,7 @@ struct lyap_ir_ctx {
     double t_newton = 0, t_res = 0, t_upd = 0;
     bool zorth = false;        // leading factor columns are orthonormal (set by the IR loop)
     bool y_diag = false;       // the Newton inner factor Y_k is diagonal (zside)
+    bool ysol_diag = false;    // the solution's Y (and the correction's Y_d) are diagonal
 };
 
 namespace {
@@ -400,7 +401,9 @@ int sol_upt(lyap_ir_ctx *h, int c, const double *Z, const double *Y, int ldy, in
     LYAP_TRY(thin_qr_F(h, p, c));
     if (Y) LYAP_TRY(nk_build_blkdiag(s, c, cd, Y, ldy, Yd, ldyd, 0, h->Nm));
     else LYAP_TRY(nk_build_blkdiag(s, c + cd, cm, nullptr, 0, nullptr, 0, 0, h->Nm));
-    LYAP_TRY(dgemm_cm(s, false, false, k, p, p, 1.0, h->Tm, k, h->Nm, p, 0.0, h->TN, k));
+    // N diagonal (the signature J, or blkdiag of diagonal Y, Y_d): T N is a column scaling
+    if (!Y || h->ysol_diag) LYAP_TRY(nk_scale_cols(s, k, p, h->Tm, k, h->Nm, p, h->TN, k));
+    else LYAP_TRY(dgemm_cm(s, false, false, k, p, p, 1.0, h->Tm, k, h->Nm, p, 0.0, h->TN, k));
     LYAP_TRY(dgemm_cm(s, false, true, k, k, p, 1.0, h->TN, k, h->Tm, k, 0.0, h->Hm, k));
     LYAP_TRY(syev_f64(s, k, h->Hm, h->wv, h->Vm, h->eig));
     int *cnt = h->ibuf + 3 * h->PW;
@@ -459,6 +462,7 @@ int ir_solve(lyap_ir_ctx *h, const double *A, const double *L, int m, const doub
     bool s_diag = false;
     if (ldlt) LYAP_TRY(is_diag_dev(h, S, m, &s_diag));
     LYAP_TRY(zside(h, ldlt, L, m, S, h->Zsol[cur], h->Ysol[cur], h->PW, &c, s_diag));
+    h->ysol_diag = s_diag;                  // afterwards every update produces a diagonal Y
     R.newton_calls = 1;
     LYAP_CUDA_TRY(cudaEventRecord(h->ev[1], s));
     LYAP_CUDA_TRY(cudaEventSynchronize(h->ev[1]));
@@ -533,6 +537,7 @@ int ir_solve(lyap_ir_ctx *h, const double *A, const double *L, int m, const doub
         tn += elapsed(h->ev[4], h->ev[5]);
         tu += elapsed(h->ev[5], h->ev[6]);
         if (2 * cn + m > h->PW) return cap_fail(__LINE__, 2 * cn + m, h->PW);
+        h->ysol_diag = true;                // the update's Y is diag(selected eigenvalues)
         cur = nxt;
         c = cn;
         R.steps = i;
@@ -744,6 +749,10 @@ int lyap_res_fac_chol(lyap_ir_handle h, const double *A, const double *L, int m,
 int lyap_sol_upt_ldlt(lyap_ir_handle h, int c, const double *Z, const double *Y, int cd, const double *Zd,
                       const double *Yd, double eta_s, double *Zn, double *Yn, int *r) {
     if (!h || !Z || !Y || !Zd || !Yd || !Zn || !Yn || !r) return LYAP_ERR_ARG;
+    bool d1 = false, d2 = false;
+    LYAP_TRY(is_diag_dev(h, Y, c, &d1));
+    LYAP_TRY(is_diag_dev(h, Yd, cd, &d2));
+    h->ysol_diag = d1 && d2;
     int rc = sol_upt(h, c, Z, Y, c, cd, Zd, Yd, cd, 0, nullptr, eta_s, Zn, Yn, c + cd, r);
     if (rc == LYAP_OK) LYAP_CUDA_TRY(cudaStreamSynchronize(h->s));
     return rc;
