@@ -540,41 +540,8 @@ __global__ void gje_prep_kernel(int n, int k, int b, int c0, int c1, T *__restri
 // block's row interchanges (the composite of the transpositions ipiv[K0..K0+nb) in
 // order), then B_outer = the pivot rows' rest entries (n x nb, K-major for the GEMM)
 // and the pivot rows' rest entries are zeroed.
-// (1) one warp: composite permutation of the touched positions -> (dst, src) list
-__global__ void gje_outer_perm_kernel(int K0, int nb, const int *__restrict__ ipiv, int *__restrict__ omoved,
-                                      int *__restrict__ onmoved)
-{
-    __shared__ int cand[2 * GJE_NB], src[2 * GJE_NB];
-    __shared__ int ncand;
-    const int ln = threadIdx.x;
-    for (int t = ln; t < nb; t += 32) { cand[t] = K0 + t; src[t] = K0 + t; }
-    if (ln == 0) ncand = nb;
-    __syncwarp();
-    for (int j = 0; j < nb; j++) {
-        const int pj = ipiv[K0 + j];
-        const int nc0 = ncand;
-        int ip = -1;
-        for (int t0 = 0; t0 < nc0 && ip < 0; t0 += 32) {
-            const unsigned hit = __ballot_sync(0xffffffffu, t0 + ln < nc0 && cand[t0 + ln] == pj);
-            if (hit) ip = t0 + __ffs(hit) - 1;
-        }
-        if (ip < 0) {
-            ip = nc0;
-            if (ln == 0) { cand[ip] = pj; src[ip] = pj; ncand = nc0 + 1; }
-        }
-        __syncwarp();
-        if (ln == 0) { const int t = src[j]; src[j] = src[ip]; src[ip] = t; }
-        __syncwarp();
-    }
-    if (ln == 0) {
-        int m = 0;
-        for (int t = 0; t < ncand; t++)
-            if (src[t] != cand[t]) { omoved[2 * m] = cand[t]; omoved[2 * m + 1] = src[t]; m++; }
-        *onmoved = m;
-    }
-}
 
-// (1') O(n) parallel alternative to the warp replay: with invprev = the inverse of rowperm
+// (1) composite permutation of the block in O(n) parallel work: with invprev = the inverse of rowperm
 // before the block and rowperm after it, position i (>= K0) now holds the row that was at
 // src = invprev[rowperm[i]].  The (dst, src) list order is irrelevant (each dst once);
 // slot_of[y] = list index of pivot row K0 + y (or -1), for the scatter.

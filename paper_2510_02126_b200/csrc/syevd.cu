@@ -411,82 +411,6 @@ tridiag_w_kernel(TridArgs a)
 #endif
 }
 
-// (previous two-barrier version kept for reference in the git history)
-__global__ void __launch_bounds__(256)
-tridiag_kernel_2sync(TridArgs a)
-{
-    cg::grid_group grid = cg::this_grid();
-    extern __shared__ double sm[];
-    double *v = sm;              // p
-    double *w = sm + a.p;        // p
-    __shared__ double red[32];
-    __shared__ double s_tau, s_beta;
-    const int p = a.p;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
-    const int gw = blockIdx.x * nwb + wid, nwg = gridDim.x * nwb;
-    double *A = a.A;
-    for (int j = 0; j + 2 < p; j++) {
-        const int L = p - j - 1;
-        const double *x = A + (long)j * p + j + 1;        // column j, rows j+1..p-1
-        double s = 0.0;
-        for (int i = 1 + threadIdx.x; i < L; i += blockDim.x) { double t = x[i]; v[i] = t; s = fma(t, t, s); }
-        s = block_sum(s, red);
-        if (threadIdx.x == 0) {
-            double alpha = x[0];
-            if (s == 0.0) { s_tau = 0.0; s_beta = alpha; }
-            else {
-                double beta = -copysign(sqrt(alpha * alpha + s), alpha);
-                s_tau = (beta - alpha) / beta;
-                s_beta = beta;
-                v[0] = alpha - beta;            // scale factor stored temporarily
-            }
-        }
-        __syncthreads();
-        const double tau = s_tau;
-        if (blockIdx.x == 0 && threadIdx.x == 0) { a.d[j] = A[(long)j * p + j]; a.e[j] = s_beta; a.tau[j] = tau; }
-        if (tau == 0.0) {
-            if (blockIdx.x == 0)        // reflector column j = 0 below the subdiagonal
-                for (int i = 1 + threadIdx.x; i < L; i += blockDim.x) A[(long)j * p + j + 1 + i] = 0.0;
-            grid.sync();
-            continue;
-        }
-        const double scale = 1.0 / v[0];
-        __syncthreads();
-        for (int i = threadIdx.x; i < L; i += blockDim.x) v[i] = (i == 0) ? 1.0 : v[i] * scale;
-        __syncthreads();
-        // p = tau * A2 v, column-distributed (A2 symmetric: row r = column r)
-        double *A2 = A + (long)(j + 1) * p + (j + 1);
-        for (int r = gw; r < L; r += nwg) {
-            const double *col = A2 + (long)r * p;
-            double dsum = 0.0;
-            for (int i = lane; i < L; i += 32) dsum = fma(col[i], v[i], dsum);
-            dsum = warp_sum(dsum);
-            if (lane == 0) a.P[r] = tau * dsum;
-        }
-        grid.sync();
-        double k = 0.0;
-        for (int i = threadIdx.x; i < L; i += blockDim.x) { double t = a.P[i]; w[i] = t; k = fma(t, v[i], k); }
-        k = 0.5 * tau * block_sum(k, red);
-        for (int i = threadIdx.x; i < L; i += blockDim.x) w[i] = fma(-k, v[i], w[i]);
-        __syncthreads();
-        for (int r = gw; r < L; r += nwg) {
-            double *col = A2 + (long)r * p;
-            const double vr = v[r], wr = w[r];
-            for (int i = lane; i < L; i += 32) col[i] = col[i] - v[i] * wr - w[i] * vr;
-        }
-        if (blockIdx.x == 0)            // store v[1..] below the subdiagonal of column j
-            for (int i = 1 + threadIdx.x; i < L; i += blockDim.x) A[(long)j * p + j + 1 + i] = v[i];
-        grid.sync();
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        if (p >= 2) {
-            a.d[p - 2] = A[(long)(p - 2) * p + p - 2];
-            a.e[p - 2] = A[(long)(p - 2) * p + p - 1];
-            a.tau[p - 2] = 0.0;
-        }
-        a.d[p - 1] = A[(long)(p - 1) * p + p - 1];
-    }
-}
 
 // ---------------------------------------------------------------- 2. divide and conquer
 // Leaf: dense eigendecomposition of the tridiagonal block [lo, hi) (size <= 32) by

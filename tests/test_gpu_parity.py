@@ -70,6 +70,33 @@ def test_invert_low_precision_bound(gpu, orc, prec, dt, n):
         assert np.linalg.norm(Xc - Xe) / np.linalg.norm(Xe) <= 10 * n * u * kappa
 
 
+@pytest.mark.parametrize("prec,dt", [("fp16", torch.float16), ("bf16", torch.bfloat16)])
+def test_invert_two_level_ragged(gpu, orc, prec, dt, monkeypatch):
+    """Two-level Gauss-Jordan (outer blocks of 256, ragged last block, look-ahead stream):
+    within the first-order bound of the exact inverse, as is the one-level sweep, and the
+    two differ only by rounding (the rank-256 update rounds the rest columns once instead
+    of after every rank-32 step)."""
+    n = 776                                                  # 256 + 256 + 256 + 8
+    rng = np.random.default_rng(776)
+    A = rng.standard_normal((n, n)) / np.sqrt(n) + 2 * np.eye(n)
+    A = orc.round_(A, prec)
+    X2 = cuda(A, dt)
+    p2 = torch.zeros(n, dtype=torch.int32, device="cuda")
+    gpu.invert(X2, p2)
+    monkeypatch.setenv("LYAP_GJE_1LEVEL", "1")
+    X1 = cuda(A, dt)
+    p1 = torch.zeros(n, dtype=torch.int32, device="cuda")
+    gpu.invert(X1, p1)
+    Xe = np.linalg.inv(A)
+    kappa = np.linalg.cond(A, "fro")
+    u = orc.unit_roundoff(prec)
+    for X in (X1, X2):
+        err = np.linalg.norm(X.double().cpu().numpy() - Xe) / np.linalg.norm(Xe)
+        assert err <= 10 * n * u * kappa
+    d = np.linalg.norm(X2.double().cpu().numpy() - X1.double().cpu().numpy()) / np.linalg.norm(Xe)
+    assert d <= 10 * n * u * kappa
+
+
 def test_invert_singular_reports(gpu):
     X = cuda(np.ones((5, 5)))
     with pytest.raises(gpu.LyapError):
