@@ -1054,7 +1054,9 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
     if (prof) cudaEventRecord(pev[1], s);
     // 2. divide and conquer on (d, e): leaves of size <= 32, power-of-two tree
     int nl = 1;
-    while ((p + nl - 1) / nl > 32) nl *= 2;
+    static int leaf = 0;
+    if (leaf == 0) { const char *e = getenv("LYAP_DC_LEAF"); leaf = e ? std::max(4, std::min(32, atoi(e))) : 16; }   // 16: measured best
+    while ((p + nl - 1) / nl > leaf) nl *= 2;
     std::vector<int> hb(nl + 1);
     for (int i = 0; i <= nl; i++) hb[i] = (int)((long)i * p / nl);
     // Cuppen tears T = diag(T1', T2') + |e| v v^T at the leaf boundaries, on the device
