@@ -157,6 +157,7 @@ struct Rrqr2Args {
     int *rank;
 };
 
+template <int RPL>
 __global__ void __launch_bounds__(256)
 rrqr2_kernel(Rrqr2Args a)
 {
@@ -193,13 +194,21 @@ rrqr2_kernel(Rrqr2Args a)
     }
     int rank = a.kmax, prev = -1;
     double r11 = 0.0, prev_alpha = 0.0;
+#ifdef LYAP_PANEL_PROF
+    long long pt[5] = {0, 0, 0, 0, 0}, tl = clock64();
+#define RPROF(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) { long long t_ = clock64(); pt[i] += t_ - tl; tl = t_; } } while (0)
+#else
+#define RPROF(i) do { } while (0)
+#endif
     for (int j = 0; j < a.kmax; j++) {
         grid.sync();
+        RPROF(0);
         const int buf = j & 1;
         const double *bs = a.bsum + buf * G, *bb = a.bbest + buf * G;
         const int *bx = a.bidx + buf * G;
         // ---- every CTA: identical reduction of the partials, stop test, pivot
         double t = 0.0, bv = -1.0; int bi = n;
+#pragma unroll 4
         for (int b = lane; b < G; b += 32) {
             t += bs[b];
             const double v = bb[b]; const int i2 = bx[b];
@@ -219,6 +228,7 @@ rrqr2_kernel(Rrqr2Args a)
             double *xp = a.M + (long)prev * c;
             for (int i = j - 1 + lane; i < c; i += 32) xp[i] = (i == j - 1) ? prev_alpha : 0.0;
         }
+        RPROF(1);
         if (stop) { rank = j; break; }
         const int pc = bi;
         // ---- reflector of column pc, rows j..c-1, in shared memory
@@ -240,37 +250,74 @@ rrqr2_kernel(Rrqr2Args a)
         if (j == 0) r11 = fabs(alpha);
         if (blockIdx.x == 0 && threadIdx.x == 0) { a.perm[j] = pc; if (j == 0) a.scal[0] = fabs(alpha); }
         __syncthreads();
+        RPROF(2);
         // ---- owners: apply H_j to active columns, downdate norms, next partials
         double bsum = 0.0, bbest = -1.0; int bidx = n;
         for (int col = gw; col < n; col += nwg) {
             if (col == pc) { if (lane == 0) a.active[col] = 0; continue; }
             if (!a.active[col]) continue;
             double *y = a.M + (long)col * c;
-            double d = 0.0;
-            if (vtv != 0.0) {
-                for (int i = j + lane; i < c; i += 32) d = fma(vsh[i], y[i], d);
-                d = warp_sum(d);
-                const double f = 2.0 * d / vtv;
-                for (int i = j + lane; i < c; i += 32) y[i] = fma(-f, vsh[i], y[i]);
-                __syncwarp();
-            }
-            const double yj = y[j];
-            double s2 = a.nrm2[col];
-            const double r = (s2 > 0.0) ? 1.0 - (yj * yj) / s2 : 0.0;
-            const double temp = fmax(r, 0.0);
-            const double temp2 = temp * (s2 / fmax(a.nrm0[col], 1e-300));
-            if (temp2 <= 1.5e-8) {                     // sqrt(eps) rule: recompute exactly
-                double e = 0.0;
-                for (int i = j + 1 + lane; i < c; i += 32) e = fma(y[i], y[i], e);
-                s2 = warp_sum(e);
-                if (lane == 0) a.nrm0[col] = s2;
+            double yj, s2 = a.nrm2[col];
+            if constexpr (RPL > 0) {
+                // the column's active rows in registers: all loads in flight at once, one
+                // load and one store per element
+                double yr[RPL];
+#pragma unroll
+                for (int u = 0; u < RPL; u++) { const int i = j + lane + 32 * u; yr[u] = (i < c) ? y[i] : 0.0; }
+                if (vtv != 0.0) {
+                    double d = 0.0;
+#pragma unroll
+                    for (int u = 0; u < RPL; u++) { const int i = j + lane + 32 * u; if (i < c) d = fma(vsh[i], yr[u], d); }
+                    d = warp_sum(d);
+                    const double f = 2.0 * d / vtv;
+#pragma unroll
+                    for (int u = 0; u < RPL; u++) {
+                        const int i = j + lane + 32 * u;
+                        if (i < c) { yr[u] = fma(-f, vsh[i], yr[u]); y[i] = yr[u]; }
+                    }
+                }
+                yj = __shfl_sync(0xffffffffu, yr[0], 0);
+                const double r = (s2 > 0.0) ? 1.0 - (yj * yj) / s2 : 0.0;
+                const double temp2 = fmax(r, 0.0) * (s2 / fmax(a.nrm0[col], 1e-300));
+                if (temp2 <= 1.5e-8) {                 // sqrt(eps) rule: recompute exactly
+                    double e = 0.0;
+#pragma unroll
+                    for (int u = 0; u < RPL; u++) { const int i = j + lane + 32 * u; if (i > j && i < c) e = fma(yr[u], yr[u], e); }
+                    s2 = warp_sum(e);
+                    if (lane == 0) a.nrm0[col] = s2;
+                } else {
+                    s2 = s2 - yj * yj;
+                }
             } else {
-                s2 = s2 - yj * yj;
+                double d = 0.0;
+                if (vtv != 0.0) {
+#pragma unroll 8
+                    for (int i = j + lane; i < c; i += 32) d = fma(vsh[i], y[i], d);
+                    d = warp_sum(d);
+                    const double f = 2.0 * d / vtv;
+#pragma unroll 8
+                    for (int i = j + lane; i < c; i += 32) y[i] = fma(-f, vsh[i], y[i]);
+                    __syncwarp();
+                }
+                yj = y[j];
+                const double r = (s2 > 0.0) ? 1.0 - (yj * yj) / s2 : 0.0;
+                const double temp = fmax(r, 0.0);
+                const double temp2 = temp * (s2 / fmax(a.nrm0[col], 1e-300));
+                if (temp2 <= 1.5e-8) {                 // sqrt(eps) rule: recompute exactly
+                    double e = 0.0;
+#pragma unroll 8
+                    for (int i = j + 1 + lane; i < c; i += 32) e = fma(y[i], y[i], e);
+                    s2 = warp_sum(e);
+                    if (lane == 0) a.nrm0[col] = s2;
+                } else {
+                    s2 = s2 - yj * yj;
+                }
             }
             if (lane == 0) a.nrm2[col] = s2;
             bsum += s2;
             if (s2 > bbest || (s2 == bbest && col < bidx)) { bbest = s2; bidx = col; }
         }
+        RPROF(3);
         prev = pc; prev_alpha = alpha;
         if (lane == 0) { s_sum[wib] = bsum; s_best[wib] = bbest; s_idx[wib] = bidx; }
         __syncthreads();
@@ -292,6 +339,11 @@ rrqr2_kernel(Rrqr2Args a)
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.rank = rank;
+#ifdef LYAP_PANEL_PROF
+    if (blockIdx.x == 0 && threadIdx.x == 0 && rank > 0)
+        printf("rrqr2 n=%d c=%d grid=%d rank=%d cycles/step: gridsync %lld pivot %lld reflector %lld apply %lld\n", n, c,
+               gridDim.x, rank, pt[0] / rank, pt[1] / rank, pt[2] / rank, pt[3] / rank);
+#endif
 }
 
 // Zout(col, r) = M[col][r] for r < k, rounded to prec (physical columns = rows of Z)
@@ -355,8 +407,10 @@ int rank_trunc_chol_f64(cudaStream_t s, int n, int c, const double *Z, double to
         max_blocks = nsm * (per < 2 ? per : 2);
         if (max_blocks > 1024) max_blocks = 1024;
         if (max_blocks < 1) max_blocks = 1;
-        cudaFuncSetAttribute(rrqr2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, rrqr2_kernel, 256, 48 * 1024);
+        for (void *f : {(void *)rrqr2_kernel<0>, (void *)rrqr2_kernel<16>, (void *)rrqr2_kernel<32>,
+                        (void *)rrqr2_kernel<64>})
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, rrqr2_kernel<64>, 256, 48 * 1024);
         max_blocks2 = nsm * std::max(1, std::min(per2, 1));
         if (max_blocks2 > 512) max_blocks2 = 512;
     }
@@ -367,8 +421,12 @@ int rank_trunc_chol_f64(cudaStream_t s, int n, int c, const double *Z, double to
                      scal, rank};
         void *args2[] = {&a2};
         KTimer kt(KC_RRQR, s);
-        LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)rrqr2_kernel, dim3(grid), dim3(256), args2,
-                                                  sizeof(double) * (size_t)c, s));
+        // the register-resident column variant measured slower (occupancy); keep it selectable
+        void *fn = (void *)rrqr2_kernel<0>;
+        if (env_flag("LYAP_RRQR_REG"))
+            fn = (c <= 512) ? (void *)rrqr2_kernel<16> : (c <= 1024) ? (void *)rrqr2_kernel<32>
+               : (c <= 2048) ? (void *)rrqr2_kernel<64> : (void *)rrqr2_kernel<0>;
+        LYAP_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args2, sizeof(double) * (size_t)c, s));
     } else {
         const int grid = want < max_blocks ? want : max_blocks;
         RrqrArgs a{n, c, c < n ? c : n, tol, w.M, w.nrm, bsum, bbest, bidx, perm, v, scal, rank};

@@ -10,8 +10,10 @@ if cfg.startswith("cfg4"):                      # cfg4:<index> -- one member of 
     p = P.cfg4_member(int(cfg.split(":")[1]) if ":" in cfg else 0)
     wl = dict(us="fp16", tol=1e-14, maxit=30, max_cols=1536)
 else:
-    wl = WORKLOADS[cfg]
+    wl = dict(WORKLOADS[cfg])
     p = getattr(P, wl["gen"])()
+if len(sys.argv) > 3:
+    wl["us"] = sys.argv[3]                      # solver precision override (e.g. cfg2 fp32)
 mc = int(sys.argv[2]) if len(sys.argv) > 2 else wl["max_cols"]
 A = torch.tensor(p.A, dtype=torch.float64, device="cuda")
 Lt = torch.tensor(np.ascontiguousarray(p.L.T), dtype=torch.float64, device="cuda")

@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2510_02126_b200 as G
 ns = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1024,4096").split(",")]
-dt = {"bf16": torch.bfloat16, "fp16": torch.float16}[sys.argv[2] if len(sys.argv) > 2 else "bf16"]
+dt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[sys.argv[2] if len(sys.argv) > 2 else "bf16"]
 for n in ns:
     g = torch.Generator(device="cuda").manual_seed(n)
     A0 = (torch.randn(n, n, device="cuda", generator=g) / n ** 0.5 - 2 * torch.eye(n, device="cuda")).to(dt)
@@ -18,10 +18,12 @@ for n in ns:
     ms = e0.elapsed_time(e1) / reps
     res = (A0.double() @ A.double() - torch.eye(n, device="cuda", dtype=torch.float64)).norm() / n ** 0.5
     print(f"invert n={n} {dt}: {ms:8.2f} ms  {2 * n ** 3 / ms / 1e9:8.2f} TFLOP/s (2n^3)  resid {res:.2e}")
-    for cls in ("gje_panel", "gje_update", "tc_gemm"):
+    for cls in ("gje_panel", "gje_update", "tc_gemm", "dgemm"):
         G.kernel_timing(cls); A.copy_(A0); G.invert(A); t, c = G.kernel_stats()[:2]
         print(f"   {cls:10s} {t:8.2f} ms {c:6d} launches")
     G.kernel_timing(None)
+    if dt == torch.float32:
+        continue
     for K in (32, 256):
         X = torch.randn(n, K, device="cuda").to(dt); B = torch.randn(n, K, device="cuda").to(dt)
         C = torch.zeros(n, n, device="cuda", dtype=dt)
