@@ -158,7 +158,7 @@ struct Rrqr2Args {
 };
 
 template <int RPL>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, RPL == 0 ? 2 : 1)
 rrqr2_kernel(Rrqr2Args a)
 {
     cg::grid_group grid = cg::this_grid();
@@ -410,8 +410,8 @@ int rank_trunc_chol_f64(cudaStream_t s, int n, int c, const double *Z, double to
         for (void *f : {(void *)rrqr2_kernel<0>, (void *)rrqr2_kernel<16>, (void *)rrqr2_kernel<32>,
                         (void *)rrqr2_kernel<64>})
             cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, rrqr2_kernel<64>, 256, 48 * 1024);
-        max_blocks2 = nsm * std::max(1, std::min(per2, 1));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, rrqr2_kernel<0>, 256, 48 * 1024);
+        max_blocks2 = nsm * std::max(1, std::min(per2, 2));     // two CTAs per SM: half the columns per warp
         if (max_blocks2 > 512) max_blocks2 = 512;
     }
     const int want = ceil_div(n, 8);
