@@ -49,6 +49,7 @@ extern "C" {
 #define LYAP_STATUS_STAGNATED 1
 #define LYAP_STATUS_MAXSTEPS  2
 #define LYAP_STATUS_SOLVER_FAILED 3
+#define LYAP_STATUS_CAPACITY  4   /* refinement stopped: the next factor would exceed max_cols */
 
 /* Algorithmic parameters (Section 4.1 l.1419-1428 for defaults). */
 typedef struct {
@@ -105,8 +106,10 @@ int lyap_ir_destroy(lyap_ir_handle h);
  *   Y  device, column-major max_cols x max_cols fp64 (output; LDL^T only,
  *      leading *rank x *rank block, diagonal) or NULL
  *   rep  host pointer or NULL.
- * Errors: ARG, CUDA, CAPACITY; solver breakdowns are reported in
- * rep->status = LYAP_STATUS_SOLVER_FAILED with the best iterate returned. */
+ * Errors: ARG, CUDA, CAPACITY (only if the initial solve does not fit); solver
+ * breakdowns are reported in rep->status = LYAP_STATUS_SOLVER_FAILED, and a factor
+ * outgrowing max_cols later in rep->status = LYAP_STATUS_CAPACITY, both with the last
+ * iterate returned. */
 int lyap_ir_solve(lyap_ir_handle h, const double *A, const double *L, int m,
                   const double *S, int ur, double tol, int maxit,
                   double *Z, double *Y, int *rank, lyap_ir_report *rep);

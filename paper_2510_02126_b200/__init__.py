@@ -24,7 +24,7 @@ _lib = None
 
 FP64, FP32, FP16, BF16 = 0, 1, 2, 3
 PREC = {"fp64": FP64, "fp32": FP32, "fp16": FP16, "bf16": BF16}
-STATUS = {0: "converged", 1: "stagnated", 2: "max_steps", 3: "solver_failure"}
+STATUS = {0: "converged", 1: "stagnated", 2: "max_steps", 3: "solver_failure", 4: "capacity"}
 ERRORS = {-1: "invalid argument", -2: "CUDA error / no device", -3: "singular matrix",
           -4: "overflow in solver precision", -5: "capacity exceeded"}
 

@@ -518,25 +518,38 @@ int ir_solve(lyap_ir_ctx *h, const double *A, const double *L, int m, const doub
             if (rc != LYAP_OK) { R.status = LYAP_STATUS_SOLVER_FAILED; break; }
         }
         int cd = 0, cm = 0;
+        // a factor outgrowing the handle's capacity ends the refinement with the last
+        // iterate (LYAP_STATUS_CAPACITY) instead of an error
+        int rcz = LYAP_OK;
         if (ldlt) {
-            LYAP_TRY(zside(h, true, h->Ld, r, h->Sd, h->Zdel, h->Ydel, h->PZ, &cd, true));   // Sd diagonal
+            rcz = zside(h, true, h->Ld, r, h->Sd, h->Zdel, h->Ydel, h->PZ, &cd, true);   // Sd diagonal
         } else {
-            if (r > 0) LYAP_TRY(zside(h, false, h->Ld, r, nullptr, h->Zdel, nullptr, 0, &cd, false));
-            if (rmm > 0) LYAP_TRY(zside(h, false, h->Lm, rmm, nullptr, h->Zdel2, nullptr, 0, &cm, false));
+            if (r > 0) rcz = zside(h, false, h->Ld, r, nullptr, h->Zdel, nullptr, 0, &cd, false);
+            if (rcz == LYAP_OK && rmm > 0) rcz = zside(h, false, h->Lm, rmm, nullptr, h->Zdel2, nullptr, 0, &cm, false);
         }
+        if (rcz == LYAP_ERR_CAPACITY) { R.status = LYAP_STATUS_CAPACITY; break; }
+        LYAP_TRY(rcz);
         R.newton_calls++;
         LYAP_CUDA_TRY(cudaEventRecord(h->ev[5], s));
         // ---- solution update at u_c = fp64
         int cn = 0;
         const int nxt = 1 - cur;
-        LYAP_TRY(sol_upt(h, c, h->Zsol[cur], ldlt ? h->Ysol[cur] : nullptr, h->PW, cd, h->Zdel,
-                         ldlt ? h->Ydel : nullptr, h->PZ, cm, h->Zdel2, h->opt.eta_s, h->Zsol[nxt], h->Ysol[nxt],
-                         h->PW, &cn));
+        const int rcu = sol_upt(h, c, h->Zsol[cur], ldlt ? h->Ysol[cur] : nullptr, h->PW, cd, h->Zdel,
+                                ldlt ? h->Ydel : nullptr, h->PZ, cm, h->Zdel2, h->opt.eta_s, h->Zsol[nxt],
+                                h->Ysol[nxt], h->PW, &cn);
+        if (rcu == LYAP_ERR_CAPACITY) { R.status = LYAP_STATUS_CAPACITY; break; }
+        LYAP_TRY(rcu);
         LYAP_CUDA_TRY(cudaEventRecord(h->ev[6], s));
         LYAP_CUDA_TRY(cudaEventSynchronize(h->ev[6]));
         tn += elapsed(h->ev[4], h->ev[5]);
         tu += elapsed(h->ev[5], h->ev[6]);
-        if (2 * cn + m > h->PW) return cap_fail(__LINE__, 2 * cn + m, h->PW);
+        if (2 * cn + m > h->PW || cn > h->cmax) {
+            // the update is valid but the next residual (or the output) would not fit:
+            // keep the last verified iterate
+            R.status = LYAP_STATUS_CAPACITY;
+            if (verbose()) fprintf(stderr, "lyap: stop at step %d: rank %d exceeds the capacity\n", i, cn);
+            break;
+        }
         h->ysol_diag = true;                // the update's Y is diag(selected eigenvalues)
         cur = nxt;
         c = cn;

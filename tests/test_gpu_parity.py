@@ -338,3 +338,17 @@ def test_ir_cfg1_full_size(gpu, orc):
     assert res.report["steps"] == ro.steps
     assert orc.rel_residual_explicit(p.A, Xg, W) <= 1e-13
     assert np.linalg.norm(Xg - Xo) <= 1e-10 * np.linalg.norm(Xo)
+
+
+def test_ir_capacity_stop_returns_last_iterate(gpu, orc):
+    """A factor outgrowing max_cols ends the refinement with status "capacity" and the
+    last verified iterate (not an error): its explicit residual matches the reported one."""
+    p = P.cfg0()
+    s = gpu.Solver(p.n, us="fp16", max_cols=40)
+    res = s.solve(cuda(p.A), colmajor(p.L), None, tol=1e-14, maxit=10)
+    rep = res.report
+    assert rep["status"] in ("capacity", "converged")
+    if rep["status"] == "capacity":
+        Xg = _X(res.Z, res.Y)
+        r_exp = orc.rel_residual_explicit(p.A, Xg, p.W())
+        assert np.isfinite(r_exp) and r_exp <= 10 * rep["res"][0]
