@@ -358,7 +358,10 @@ qr_panel_cluster_kernel(int m, int j0, int jb, int RB, double *__restrict__ W, d
 //     s' = S_xx - 2 f S_vx + f^2 S_vv   (f = tau d_{j+1}),
 // which is used only when s' >= S_xx / 2 (no cancellation: error a few ulp);
 // otherwise a second exchange computes s' directly.
-constexpr int QRT = 256, QNV = QB + 5;     // 32 dots + S_xx, S_vx, S_vv, x_{j+1}, v_{j+1}
+constexpr int QRT = 256, QNV = QB + 5;
+#ifdef LYAP_PANEL_PROF
+__device__ unsigned long long g_qr_fallbacks = 0, g_qr_reflectors = 0;
+#endif     // 32 dots + S_xx, S_vx, S_vv, x_{j+1}, v_{j+1}
 
 template <int NV>
 __device__ __forceinline__ void qr_cta_reduce_push(double (&vals)[NV], int lane, int wid, int q, int NC,
@@ -429,6 +432,9 @@ qr_panel_reg_kernel(int m, int j0, int jb, double *__restrict__ W, double *__res
     }
     for (int jj = 0; jj < jb; jj++) {
         const int buf = jj & 1;
+#ifdef LYAP_PANEL_PROF
+        if (q == 0 && tid == 0) atomicAdd(&g_qr_reflectors, 1ull);
+#endif
         double tj = 0.0, v0 = 0.0, alpha = 0.0;
         const double nrm2 = s + x0 * x0;
         if (nrm2 != 0.0) {
@@ -478,6 +484,9 @@ qr_panel_reg_kernel(int m, int j0, int jb, double *__restrict__ W, double *__res
             if (sd >= 0.5 * sxx) {
                 s = sd;
             } else {
+#ifdef LYAP_PANEL_PROF
+                if (q == 0 && tid == 0) atomicAdd(&g_qr_fallbacks, 1ull);
+#endif
                 const double xv = sel_col32(row, jj + 1);
                 double v2[2] = {below ? xv * xv : 0.0, 0.0};
                 v2[0] = warp_sum(v2[0]);
@@ -687,6 +696,13 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
 
 }  // namespace lyap
 
+#ifdef LYAP_PANEL_PROF
+extern "C" void lyap_debug_qr_counters(unsigned long long *fb, unsigned long long *refl)
+{
+    cudaMemcpyFromSymbol(fb, lyap::g_qr_fallbacks, sizeof(*fb));
+    cudaMemcpyFromSymbol(refl, lyap::g_qr_reflectors, sizeof(*refl));
+}
+#endif
 extern "C" int lyap_qr(int m, int n, const double *A, double *Q, double *R, void *stream)
 {
     using namespace lyap;
