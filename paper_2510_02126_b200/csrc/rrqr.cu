@@ -158,7 +158,7 @@ struct Rrqr2Args {
 };
 
 template <int RPL>
-__global__ void __launch_bounds__(256, RPL == 0 ? 2 : 1)
+__global__ void __launch_bounds__(256, RPL == 0 ? 4 : 2)
 rrqr2_kernel(Rrqr2Args a)
 {
     cg::grid_group grid = cg::this_grid();
@@ -169,15 +169,20 @@ rrqr2_kernel(Rrqr2Args a)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
     const int gw = blockIdx.x * nwb + wib, nwg = gridDim.x * nwb;
     const int n = a.n, c = a.c, G = gridDim.x;
+    // Owned columns col = gw + t nwg (t < 32): lane t keeps that column's trailing norm^2,
+    // its norm^2 at the last exact recomputation and its active flag in registers (no
+    // global metadata loads in front of the column loads).
+    double m_n2 = 0.0, m_n0 = 0.0;
+    bool m_act = false;
     // initial norms (rows 0..c-1), partials of step 0
     {
         double bsum = 0.0, bbest = -1.0; int bidx = n;
-        for (int col = gw; col < n; col += nwg) {
+        for (int col = gw, t = 0; col < n; col += nwg, t++) {
             const double *x = a.M + (long)col * c;
             double s = 0.0;
             for (int i = lane; i < c; i += 32) s = fma(x[i], x[i], s);
             s = warp_sum(s);
-            if (lane == 0) { a.nrm2[col] = s; a.nrm0[col] = s; a.active[col] = 1; }
+            if (lane == t) { m_n2 = s; m_n0 = s; m_act = true; }
             bsum += s;
             if (s > bbest || (s == bbest && col < bidx)) { bbest = s; bidx = col; }
         }
@@ -206,21 +211,30 @@ rrqr2_kernel(Rrqr2Args a)
         const int buf = j & 1;
         const double *bs = a.bsum + buf * G, *bb = a.bbest + buf * G;
         const int *bx = a.bidx + buf * G;
-        // ---- every CTA: identical reduction of the partials, stop test, pivot
-        double t = 0.0, bv = -1.0; int bi = n;
+        // ---- every CTA: identical reduction of the partials (warp 0 only: the G partials are
+        // the same few L2 lines for every CTA), stop test, pivot
+        __shared__ double s_t;
+        __shared__ int s_bi;
+        if (wib == 0) {
+            double t = 0.0, bv = -1.0; int bi = n;
 #pragma unroll 4
-        for (int b = lane; b < G; b += 32) {
-            t += bs[b];
-            const double v = bb[b]; const int i2 = bx[b];
-            if (v > bv || (v == bv && i2 < bi)) { bv = v; bi = i2; }
-        }
-        t = warp_sum(t);
+            for (int b = lane; b < G; b += 32) {
+                t += bs[b];
+                const double v = bb[b]; const int i2 = bx[b];
+                if (v > bv || (v == bv && i2 < bi)) { bv = v; bi = i2; }
+            }
+            t = warp_sum(t);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; }
+            }
+            if (lane == 0) { s_t = t; s_bi = bi; }
         }
+        __syncthreads();
+        const double t = s_t;
+        const int bi = s_bi;
         const double tr = sqrt(t);
         const bool stop = (j > 0 && tr <= a.tol * r11) || tr == 0.0 || bi >= n;
         // owners finalise the previous pivot column (all CTAs have finished reading it)
@@ -253,11 +267,12 @@ rrqr2_kernel(Rrqr2Args a)
         RPROF(2);
         // ---- owners: apply H_j to active columns, downdate norms, next partials
         double bsum = 0.0, bbest = -1.0; int bidx = n;
-        for (int col = gw; col < n; col += nwg) {
-            if (col == pc) { if (lane == 0) a.active[col] = 0; continue; }
-            if (!a.active[col]) continue;
+        for (int col = gw, t = 0; col < n; col += nwg, t++) {
+            if (col == pc) { if (lane == t) m_act = false; continue; }
+            if (!__shfl_sync(0xffffffffu, (int)m_act, t)) continue;
             double *y = a.M + (long)col * c;
-            double yj, s2 = a.nrm2[col];
+            double yj, s2 = __shfl_sync(0xffffffffu, m_n2, t);
+            const double n0 = __shfl_sync(0xffffffffu, m_n0, t);
             if constexpr (RPL > 0) {
                 // the column's active rows in registers: all loads in flight at once, one
                 // load and one store per element
@@ -278,13 +293,13 @@ rrqr2_kernel(Rrqr2Args a)
                 }
                 yj = __shfl_sync(0xffffffffu, yr[0], 0);
                 const double r = (s2 > 0.0) ? 1.0 - (yj * yj) / s2 : 0.0;
-                const double temp2 = fmax(r, 0.0) * (s2 / fmax(a.nrm0[col], 1e-300));
+                const double temp2 = fmax(r, 0.0) * (s2 / fmax(n0, 1e-300));
                 if (temp2 <= 1.5e-8) {                 // sqrt(eps) rule: recompute exactly
                     double e = 0.0;
 #pragma unroll
                     for (int u = 0; u < RPL; u++) { const int i = j + lane + 32 * u; if (i > j && i < c) e = fma(yr[u], yr[u], e); }
                     s2 = warp_sum(e);
-                    if (lane == 0) a.nrm0[col] = s2;
+                    if (lane == t) m_n0 = s2;
                 } else {
                     s2 = s2 - yj * yj;
                 }
@@ -302,18 +317,18 @@ rrqr2_kernel(Rrqr2Args a)
                 yj = y[j];
                 const double r = (s2 > 0.0) ? 1.0 - (yj * yj) / s2 : 0.0;
                 const double temp = fmax(r, 0.0);
-                const double temp2 = temp * (s2 / fmax(a.nrm0[col], 1e-300));
+                const double temp2 = temp * (s2 / fmax(n0, 1e-300));
                 if (temp2 <= 1.5e-8) {                 // sqrt(eps) rule: recompute exactly
                     double e = 0.0;
 #pragma unroll 8
                     for (int i = j + 1 + lane; i < c; i += 32) e = fma(y[i], y[i], e);
                     s2 = warp_sum(e);
-                    if (lane == 0) a.nrm0[col] = s2;
+                    if (lane == t) m_n0 = s2;
                 } else {
                     s2 = s2 - yj * yj;
                 }
             }
-            if (lane == 0) a.nrm2[col] = s2;
+            if (lane == t) m_n2 = s2;
             bsum += s2;
             if (s2 > bbest || (s2 == bbest && col < bidx)) { bbest = s2; bidx = col; }
         }
@@ -398,9 +413,9 @@ int rank_trunc_chol_f64(cudaStream_t s, int n, int c, const double *Z, double to
     transpose_init_kernel<<<ceil_div(tot, 256) < 2048 ? ceil_div(tot, 256) : 2048, 256, 0, s>>>(n, c, Z, w.M, perm);
     LYAP_TRY(launched());
     const bool v2 = !env_flag("LYAP_RRQR_V1");
-    static int max_blocks = 0, max_blocks2 = 0;
+    static int max_blocks = 0, nsm = 0;
     if (max_blocks == 0) {
-        int dev, nsm, per, per2;
+        int dev, per;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_kernel, 256, 0);
@@ -408,25 +423,35 @@ int rank_trunc_chol_f64(cudaStream_t s, int n, int c, const double *Z, double to
         if (max_blocks > 1024) max_blocks = 1024;
         if (max_blocks < 1) max_blocks = 1;
         for (void *f : {(void *)rrqr2_kernel<0>, (void *)rrqr2_kernel<16>, (void *)rrqr2_kernel<32>,
-                        (void *)rrqr2_kernel<64>})
+                        (void *)rrqr2_kernel<48>})
             cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, rrqr2_kernel<0>, 256, 48 * 1024);
-        max_blocks2 = nsm * std::max(1, std::min(per2, 2));     // two CTAs per SM: half the columns per warp
-        if (max_blocks2 > 512) max_blocks2 = 512;
     }
     const int want = ceil_div(n, 8);
-    if (v2 && (size_t)c * sizeof(double) <= 160 * 1024) {
-        const int grid = std::max(1, std::min(want, max_blocks2));
+    const size_t smem2 = sizeof(double) * (size_t)c;
+    // register-resident columns (one load and one store per element, all loads of a column in
+    // flight at once) up to 16 rows per lane (two CTAs per SM); streamed columns above (64
+    // registers, up to four CTAs per SM).  32 / 48 rows per lane spill: measured slower.
+    void *fn = (c <= 512) ? (void *)rrqr2_kernel<16> : (void *)rrqr2_kernel<0>;
+    if (env_flag("LYAP_RRQR_STREAM")) fn = (void *)rrqr2_kernel<0>;
+    if (env_flag("LYAP_RRQR_REG"))
+        fn = (c <= 1024) ? (void *)rrqr2_kernel<32> : (c <= 1536) ? (void *)rrqr2_kernel<48> : fn;
+    int per2 = 0;
+    if (v2 && smem2 <= 160 * 1024) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, fn, 256, smem2);
+    const int cap = (fn == (void *)rrqr2_kernel<0> && !env_flag("LYAP_RRQR_2CTA")) ? 4 : 2;
+    // at most 512 CTAs: the double-buffered partial arrays hold 2 x 512 entries
+    const int max_blocks2 = std::min(512, nsm * std::min(per2, cap));
+    if (v2 && max_blocks2 > 0 && n <= 32 * 8 * max_blocks2) {
+        // the step time is set by the warps owning the most columns: take the fewest CTAs
+        // that keep that maximum minimal (fewer partials, cheaper barrier; measured: n = 4096,
+        // 256 CTAs x 2 columns/warp 17 us/step vs 296 CTAs x 1-2 columns/warp 23 us/step)
+        const int cpw = ceil_div(n, 8 * max_blocks2);
+        int grid = std::max(1, std::min(ceil_div(n, 8 * cpw), max_blocks2));
+        if (const char *e = getenv("LYAP_RRQR_GRID")) grid = std::max(1, std::min(atoi(e), max_blocks2));
         Rrqr2Args a2{n, c, c < n ? c : n, tol, w.M, w.nrm, w.nrm + n, bsum, bbest, bidx, perm, w.ints + w.nmax + 2048 + 8,
                      scal, rank};
         void *args2[] = {&a2};
         KTimer kt(KC_RRQR, s);
-        // the register-resident column variant measured slower (occupancy); keep it selectable
-        void *fn = (void *)rrqr2_kernel<0>;
-        if (env_flag("LYAP_RRQR_REG"))
-            fn = (c <= 512) ? (void *)rrqr2_kernel<16> : (c <= 1024) ? (void *)rrqr2_kernel<32>
-               : (c <= 2048) ? (void *)rrqr2_kernel<64> : (void *)rrqr2_kernel<0>;
-        LYAP_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args2, sizeof(double) * (size_t)c, s));
+        LYAP_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args2, smem2, s));
     } else {
         const int grid = want < max_blocks ? want : max_blocks;
         RrqrArgs a{n, c, c < n ? c : n, tol, w.M, w.nrm, bsum, bbest, bidx, perm, v, scal, rank};
@@ -444,7 +469,7 @@ int rank_trunc_chol_f64(cudaStream_t s, int n, int c, const double *Z, double to
         return LYAP_OK;
     }
     long to = (long)n * k;
-    if (v2 && (size_t)c * sizeof(double) <= 160 * 1024)
+    if (v2 && max_blocks2 > 0 && n <= 32 * 8 * max_blocks2)
         rrqr2_out_kernel<<<ceil_div(to, 256) < 2048 ? ceil_div(to, 256) : 2048, 256, 0, s>>>(n, c, k, w.M, prec_out, Zout);
     else
         rrqr_out_kernel<<<ceil_div(to, 256) < 2048 ? ceil_div(to, 256) : 2048, 256, 0, s>>>(n, c, k, w.M, perm, prec_out, Zout);
