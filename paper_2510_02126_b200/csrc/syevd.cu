@@ -56,6 +56,9 @@ __device__ void make_reflector(const double *x, int L, double *v, double *red, d
     __syncthreads();
 }
 
+#ifndef TRID_CHUNK
+#define TRID_CHUNK 16
+#endif
 // One grid barrier per column: column g of the trailing matrix is owned by warp g mod
 // (#warps) for the whole reduction, so the owner's update of step j and its product with
 // v_{j+1} for step j+1 are fused (each column read and written once per step); only the
@@ -122,10 +125,20 @@ tridiag_kernel(TridArgs a)
             const int ig = g - r0;
             const double vg = v[ig], wg = w[ig];
             double s = 0.0;
-            for (int i = 1 + lane; i < L; i += 32) {
-                double x = col[i] - v[i] * wg - w[i] * vg;
-                col[i] = x;
-                s = fma(x, vn[i - 1], s);
+            // explicit chunks: all loads of a chunk in flight before its stores
+            for (int i0 = 1 + lane; i0 < L; i0 += 32 * TRID_CHUNK) {
+                double xr[TRID_CHUNK];
+#pragma unroll
+                for (int u = 0; u < TRID_CHUNK; u++) { const int i = i0 + 32 * u; if (i < L) xr[u] = col[i]; }
+#pragma unroll
+                for (int u = 0; u < TRID_CHUNK; u++) {
+                    const int i = i0 + 32 * u;
+                    if (i < L) {
+                        const double x = xr[u] - v[i] * wg - w[i] * vg;
+                        col[i] = x;
+                        s = fma(x, vn[i - 1], s);
+                    }
+                }
             }
             if (more) {
                 s = warp_sum(s);
@@ -1046,8 +1059,17 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
             }
             LYAP_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(grid_t), dim3(256), args, smem, s));
         } else {
-            int grid = std::min(max_blocks, std::max(1, p / 4));
-            LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)tridiag_kernel, dim3(grid), dim3(256), args, smem, s));
+            // shared memory for this p (not the capacity): up to two CTAs per SM, one warp
+            // per trailing column (the trailing block shrinks: the full grid is best)
+            const size_t smem_p = sizeof(double) * 4 * (size_t)p;
+            int dev, nsm, per = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tridiag_kernel, 256, smem_p);
+            const int maxb = nsm * std::max(1, std::min(per, env_flag("LYAP_TRIDIAG_1CTA") ? 1 : 2));
+            int grid = std::max(1, std::min(maxb, ceil_div(p - 1, 8)));
+            if (const char *e = getenv("LYAP_TRIDIAG_GRID")) grid = std::max(1, std::min(maxb, atoi(e)));
+            LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)tridiag_kernel, dim3(grid), dim3(256), args, smem_p, s));
         }
         LYAP_TRY(launched());
     }

@@ -133,7 +133,7 @@ def _eig_checks(A, w, V, tol=1e-12):
     assert np.linalg.norm(A @ V - V * w[None, :]) <= tol * scale * n
 
 
-@pytest.mark.parametrize("n", [33, 64, 131, 300, 700])
+@pytest.mark.parametrize("n", [33, 64, 131, 300, 700, 1100, 2100])
 def test_syevd_random(gpu, n):
     """Tridiagonalisation + divide-and-conquer path (n > 32) against numpy eigh and
     the defining identities A V = V diag(w), V^T V = I."""
@@ -164,6 +164,20 @@ def test_syevd_hard_spectra(gpu, kind):
     A = (A + A.T) / 2
     w, V = gpu.syev(cuda(A))
     _eig_checks(A, w.cpu().numpy(), V.cpu().numpy(), tol=1e-12)
+
+
+@pytest.mark.parametrize("n,c,r", [(700, 300, 25), (3000, 700, 6), (2500, 900, 60), (1500, 1300, 90)])
+def test_rank_trunc_chol_parity_sizes(gpu, orc, n, c, r):
+    """Register-resident (c <= 512) and streamed (c > 512, up to four CTAs per SM) QRCP
+    variants and the grid-size rule, against the oracle's RRQR (decaying spectrum)."""
+    rng = np.random.default_rng(n + c)
+    sv = np.logspace(0, -8, r)
+    Z = (rng.standard_normal((n, r)) * sv[None, :]) @ rng.standard_normal((r, c)) + 1e-12 * rng.standard_normal((n, c))
+    tol = np.sqrt(orc.unit_roundoff("fp16"))
+    Zg = gpu.rank_trunc_chol(colmajor(Z), tol, "fp64").cpu().numpy()
+    Zo = orc.rank_trunc_chol("fp64", Z, tol)
+    assert Zg.shape == Zo.shape
+    assert np.allclose(Zg, Zo, atol=1e-10 * np.abs(Zo).max())
 
 
 def test_rank_trunc_chol_parity(gpu, orc):
