@@ -250,6 +250,66 @@ __device__ __forceinline__ void row_load(Acc (&r)[BW], const Acc *src) {
     }
 }
 
+// 16-byte vectors <-> elements (raw bits; the conversions are to_acc / from_acc's)
+template <typename T> struct Vec16;
+template <> struct Vec16<__nv_bfloat16> {
+    static constexpr int E = 8;
+    __device__ __forceinline__ static void unpack(const uint4 &v, float (&o)[E]) {
+        const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            o[2 * i] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(w[i] & 0xffffu)));
+            o[2 * i + 1] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(w[i] >> 16)));
+        }
+    }
+    __device__ __forceinline__ static uint4 pack(const float (&x)[E]) {
+        unsigned w[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+            w[i] = (unsigned)__bfloat16_as_ushort(__float2bfloat16_rn(x[2 * i])) |
+                   ((unsigned)__bfloat16_as_ushort(__float2bfloat16_rn(x[2 * i + 1])) << 16);
+        return make_uint4(w[0], w[1], w[2], w[3]);
+    }
+};
+template <> struct Vec16<__half> {
+    static constexpr int E = 8;
+    __device__ __forceinline__ static void unpack(const uint4 &v, float (&o)[E]) {
+        const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            o[2 * i] = __half2float(__ushort_as_half((unsigned short)(w[i] & 0xffffu)));
+            o[2 * i + 1] = __half2float(__ushort_as_half((unsigned short)(w[i] >> 16)));
+        }
+    }
+    __device__ __forceinline__ static uint4 pack(const float (&x)[E]) {
+        unsigned w[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+            w[i] = (unsigned)__half_as_ushort(__float2half_rn(x[2 * i])) |
+                   ((unsigned)__half_as_ushort(__float2half_rn(x[2 * i + 1])) << 16);
+        return make_uint4(w[0], w[1], w[2], w[3]);
+    }
+};
+template <> struct Vec16<float> {
+    static constexpr int E = 4;
+    __device__ __forceinline__ static void unpack(const uint4 &v, float (&o)[E]) {
+        o[0] = __uint_as_float(v.x); o[1] = __uint_as_float(v.y); o[2] = __uint_as_float(v.z); o[3] = __uint_as_float(v.w);
+    }
+    __device__ __forceinline__ static uint4 pack(const float (&x)[E]) {
+        return make_uint4(__float_as_uint(x[0]), __float_as_uint(x[1]), __float_as_uint(x[2]), __float_as_uint(x[3]));
+    }
+};
+template <> struct Vec16<double> {
+    static constexpr int E = 2;
+    __device__ __forceinline__ static void unpack(const uint4 &v, double (&o)[E]) {
+        o[0] = __hiloint2double((int)v.y, (int)v.x); o[1] = __hiloint2double((int)v.w, (int)v.z);
+    }
+    __device__ __forceinline__ static uint4 pack(const double (&x)[E]) {
+        return make_uint4((unsigned)__double2loint(x[0]), (unsigned)__double2hiint(x[0]),
+                          (unsigned)__double2loint(x[1]), (unsigned)__double2hiint(x[1]));
+    }
+};
+
 template <typename T, int BW, int RPT, int NT>
 __global__ void __launch_bounds__(NT)
 gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T *__restrict__ X,
@@ -272,17 +332,43 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
     __shared__ int pivl[32];
     __shared__ int sflag;
     __shared__ Acc Ptop[32][33];
-    __shared__ Acc Lw[32 * 32], Tw[32 * 32];
+    __shared__ __align__(16) Acc Lw[32 * 32], Tw[32 * 32];
+#ifdef LYAP_PANEL_PROF
+    const long long t_start = clock64();
+#endif
     Acc row[RPT][BW];
+    constexpr int VE = Vec16<T>::E;
+    // full panels with 16-byte aligned rows: each row as BW / VE vector loads (scalar 2-byte
+    // loads of 32 strided rows per warp instruction made the load phase L1-bound)
+    const bool vec = (b == BW) && ((long)n * sizeof(T)) % 16 == 0 && ((long)k * sizeof(T)) % 16 == 0;
 #pragma unroll
     for (int h = 0; h < RPT; h++) {
         const int r = RPT * tid + h;
         const T *src = A + (long)(k + g0 + r) * n + k;
+        if (vec) {
+            if (r < nloc) {
+                uint4 v[BW / VE];
 #pragma unroll
-        for (int c = 0; c < BW; c++) row[h][c] = (r < nloc && c < b) ? to_acc<T>(src[c]) : Acc(0);
+                for (int u = 0; u < BW / VE; u++) v[u] = reinterpret_cast<const uint4 *>(src)[u];
+#pragma unroll
+                for (int u = 0; u < BW / VE; u++) {
+                    Acc o[VE];
+                    Vec16<T>::unpack(v[u], o);
+#pragma unroll
+                    for (int e = 0; e < VE; e++) row[h][u * VE + e] = o[e];
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < BW; c++) row[h][c] = Acc(0);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < BW; c++) row[h][c] = (r < nloc && c < b) ? to_acc<T>(src[c]) : Acc(0);
+        }
     }
     if (tid == 0) sflag = 0;
 #ifdef LYAP_PANEL_PROF
+    const long long t_loaded = clock64();
     long long pt[6] = {0, 0, 0, 0, 0, 0}, tl = clock64();
 #define PPROF(i) do { if (q == 0 && tid == 0) { long long t_ = clock64(); pt[i] += t_ - tl; tl = t_; } } while (0)
 #else
@@ -361,9 +447,11 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
         PPROF(5);
     }
 #ifdef LYAP_PANEL_PROF
+    const long long t_loop = clock64();
     if (q == 0 && tid == 0 && (k == 0 || k == 2048))
         printf("panel k=%d R=%d NC=%d cycles/col: argmax %lld bar1 %lld winner+pub+bar2 %lld push+csync %lld "
-               "select %lld elim %lld\n", k, R, NC, pt[0] / b, pt[1] / b, pt[2] / b, pt[3] / b, pt[4] / b, pt[5] / b);
+               "select %lld elim %lld | load %lld loop %lld\n", k, R, NC, pt[0] / b, pt[1] / b, pt[2] / b, pt[3] / b, pt[4] / b, pt[5] / b,
+               t_loaded - t_start, t_loop - t_loaded);
 #endif
     // ---- Linv = L11^{-1}, Uinv = U11^{-1}, T = Uinv Linv on CTA 0 (owns panel rows 0..b-1);
     // same recurrences and summation order as the single-CTA kernel, loops unrolled
@@ -448,6 +536,9 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
         for (int e = tid; e < 32 * 32; e += NT) { Lw[e] = rL[e]; Tw[e] = rT[e]; }
     }
     __syncthreads();
+#ifdef LYAP_PANEL_PROF
+    const long long t_tail1 = clock64();
+#endif
     // ---- X rows: own panel rows (block rows from T, rows below -L21 L11^{-1}), rows
     // above the panel split evenly over the cluster
 #pragma unroll
@@ -455,6 +546,29 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
         const int r = RPT * tid + h, gi = g0 + r;
         if (r >= nloc) continue;
         T *xr = X + (long)(k + gi) * b;
+        if (b == BW) {
+            // VE columns at a time: Lw rows as 16-byte shared loads, one 16-byte store; the
+            // per-element summation order (t ascending from 0) is the scalar loop's
+#pragma unroll
+            for (int c0 = 0; c0 < BW; c0 += VE) {
+                Acc acc[VE];
+                if (gi < b) {
+#pragma unroll
+                    for (int e = 0; e < VE; e++) acc[e] = Tw[gi * 32 + c0 + e];
+                } else {
+#pragma unroll
+                    for (int e = 0; e < VE; e++) acc[e] = Acc(0);
+#pragma unroll
+                    for (int t = 0; t < BW; t++) {
+                        const Acc m = -row[h][t];
+#pragma unroll
+                        for (int e = 0; e < VE; e++) acc[e] = fma(m, Lw[t * 32 + c0 + e], acc[e]);
+                    }
+                }
+                reinterpret_cast<uint4 *>(xr)[c0 / VE] = Vec16<T>::pack(acc);
+            }
+            continue;
+        }
         for (int c = 0; c < b; c++) {
             Acc sacc = Acc(0);
             if (gi < b) sacc = Tw[gi * 32 + c];
@@ -467,6 +581,11 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
     // rows above the panel: gje_xabove_kernel (the whole GPU), from T in global memory
     if (q == 0)
         for (int e = tid; e < 32 * 32; e += NT) Tglob[e] = Tw[e];
+#ifdef LYAP_PANEL_PROF
+    __syncthreads();
+    if (q == 0 && tid == 0 && (k == 0 || k == 2048))
+        printf("panel tail k=%d: T+copy %lld X rows %lld\n", k, t_tail1 - t_loop, clock64() - t_tail1);
+#endif
     cl.sync();                                                 // shared memory stays valid for remote readers
 }
 
