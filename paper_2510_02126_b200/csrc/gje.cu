@@ -314,7 +314,8 @@ template <typename T, int BW, int RPT, int NT>
 __global__ void __launch_bounds__(NT)
 gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T *__restrict__ X,
                          int *__restrict__ ipiv, int *__restrict__ moved, int *__restrict__ nmoved,
-                         int *__restrict__ info, typename Prec<T>::acc *__restrict__ Tglob)
+                         int *__restrict__ info, typename Prec<T>::acc *__restrict__ Tglob,
+                         typename Prec<T>::acc *__restrict__ Pg)
 {
     namespace cg = cooperative_groups;
     using Acc = typename Prec<T>::acc;
@@ -453,6 +454,22 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
                "select %lld elim %lld | load %lld loop %lld\n", k, R, NC, pt[0] / b, pt[1] / b, pt[2] / b, pt[3] / b, pt[4] / b, pt[5] / b,
                t_loaded - t_start, t_loop - t_loaded);
 #endif
+    // ---- rows below the block: their multipliers (in Acc precision) go to Pg, and
+    // gje_xabove_kernel (the whole GPU) forms X = -L21 L11^{-1} there
+#pragma unroll
+    for (int h = 0; h < RPT; h++) {
+        const int r = RPT * tid + h, gi = g0 + r;
+        if (r >= nloc || gi < b) continue;
+        Acc *pr = Pg + (long)gi * BW;
+        if constexpr (sizeof(Acc) == 4) {
+#pragma unroll
+            for (int c = 0; c < BW; c += 4)
+                *reinterpret_cast<float4 *>(pr + c) = make_float4(row[h][c], row[h][c + 1], row[h][c + 2], row[h][c + 3]);
+        } else {
+#pragma unroll
+            for (int c = 0; c < BW; c += 2) *reinterpret_cast<double2 *>(pr + c) = make_double2(row[h][c], row[h][c + 1]);
+        }
+    }
     // ---- Linv = L11^{-1}, Uinv = U11^{-1}, T = Uinv Linv on CTA 0 (owns panel rows 0..b-1);
     // same recurrences and summation order as the single-CTA kernel, loops unrolled
 #pragma unroll
@@ -529,63 +546,23 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
         __syncthreads();
         for (int hh = 0; hh < RT; hh++)
             if (ti + NW * hh < b && tc < b) Tw[(ti + NW * hh) * 32 + tc] = tval[hh];
-    }
-    cl.sync();
-    if (q != 0) {
-        const Acc *rL = cl.map_shared_rank(Lw, 0), *rT = cl.map_shared_rank(Tw, 0);
-        for (int e = tid; e < 32 * 32; e += NT) { Lw[e] = rL[e]; Tw[e] = rT[e]; }
-    }
-    __syncthreads();
+        __syncthreads();
 #ifdef LYAP_PANEL_PROF
-    const long long t_tail1 = clock64();
+        const long long t_tail1 = clock64();
 #endif
-    // ---- X rows: own panel rows (block rows from T, rows below -L21 L11^{-1}), rows
-    // above the panel split evenly over the cluster
-#pragma unroll
-    for (int h = 0; h < RPT; h++) {
-        const int r = RPT * tid + h, gi = g0 + r;
-        if (r >= nloc) continue;
-        T *xr = X + (long)(k + gi) * b;
-        if (b == BW) {
-            // VE columns at a time: Lw rows as 16-byte shared loads, one 16-byte store; the
-            // per-element summation order (t ascending from 0) is the scalar loop's
-#pragma unroll
-            for (int c0 = 0; c0 < BW; c0 += VE) {
-                Acc acc[VE];
-                if (gi < b) {
-#pragma unroll
-                    for (int e = 0; e < VE; e++) acc[e] = Tw[gi * 32 + c0 + e];
-                } else {
-#pragma unroll
-                    for (int e = 0; e < VE; e++) acc[e] = Acc(0);
-#pragma unroll
-                    for (int t = 0; t < BW; t++) {
-                        const Acc m = -row[h][t];
-#pragma unroll
-                        for (int e = 0; e < VE; e++) acc[e] = fma(m, Lw[t * 32 + c0 + e], acc[e]);
-                    }
-                }
-                reinterpret_cast<uint4 *>(xr)[c0 / VE] = Vec16<T>::pack(acc);
-            }
-            continue;
+        // block rows: X = T; T and Linv to global for gje_xabove_kernel (rows above: -A T,
+        // rows below: -L21 Linv)
+        if (tid < b) {
+            T *xr = X + (long)(k + tid) * b;
+            for (int c = 0; c < b; c++) xr[c] = from_acc<T>(Tw[tid * 32 + c]);
         }
-        for (int c = 0; c < b; c++) {
-            Acc sacc = Acc(0);
-            if (gi < b) sacc = Tw[gi * 32 + c];
-            else
-#pragma unroll
-                for (int t = 0; t < BW; t++) if (t < b) sacc = fma(-row[h][t], Lw[t * 32 + c], sacc);
-            xr[c] = from_acc<T>(sacc);
-        }
-    }
-    // rows above the panel: gje_xabove_kernel (the whole GPU), from T in global memory
-    if (q == 0)
-        for (int e = tid; e < 32 * 32; e += NT) Tglob[e] = Tw[e];
+        for (int e = tid; e < 32 * 32; e += NT) { Tglob[e] = Tw[e]; Tglob[32 * 32 + e] = Lw[e]; }
 #ifdef LYAP_PANEL_PROF
-    __syncthreads();
-    if (q == 0 && tid == 0 && (k == 0 || k == 2048))
-        printf("panel tail k=%d: T+copy %lld X rows %lld\n", k, t_tail1 - t_loop, clock64() - t_tail1);
+        __syncthreads();
+        if (tid == 0 && (k == 0 || k == 2048))
+            printf("panel tail k=%d: T %lld X block rows + publish %lld\n", k, t_tail1 - t_loop, clock64() - t_tail1);
 #endif
+    }
     cl.sync();                                                 // shared memory stays valid for remote readers
 }
 
@@ -786,7 +763,7 @@ int GjeWork::alloc(int n_, int prec_) {
     LYAP_CUDA_TRY(cudaMalloc(&B, es * (size_t)n * b));
     LYAP_CUDA_TRY(cudaMalloc(&tmp, es * (size_t)n * 2 * b));
     LYAP_CUDA_TRY(cudaMalloc(&Pglob, acc * (size_t)n * b));
-    LYAP_CUDA_TRY(cudaMalloc(&Tg, acc * 32 * 32));
+    LYAP_CUDA_TRY(cudaMalloc(&Tg, acc * 2 * 32 * 32));   // T, then Linv
     if ((prec == LYAP_FP16 || prec == LYAP_BF16) && n % 8 == 0 && n >= 2 * GJE_NB) {
         LYAP_CUDA_TRY(cudaMalloc(&Bo, es * (size_t)n * GJE_NB));
         LYAP_CUDA_TRY(cudaMalloc(&tmp2, es * (size_t)n * 2 * GJE_NB));
@@ -817,21 +794,34 @@ void GjeWork::release() {
 // X rows above the panel: X[i, :] = -A[i, k:k+b] T for i < k.  One warp per row: the
 // row's b panel entries are read once (coalesced) and broadcast by shuffles; same
 // summation order as the single-CTA kernel.
+// Rows below the block (cluster panel): X[k+gi, :] = -P[gi, :] Linv with the multipliers P
+// the panel left in Pg (Acc precision, ld BW) and Linv = Tglob[1024..]; the summation
+// order is the panel's (t ascending from 0).
 template <typename T>
 __global__ void __launch_bounds__(256)
-gje_xabove_kernel(int n, int k, int b, const T *__restrict__ A, const typename Prec<T>::acc *__restrict__ Tglob,
-                  T *__restrict__ X)
+gje_xabove_kernel(int n, int k, int b, int R, const T *__restrict__ A, const typename Prec<T>::acc *__restrict__ Tglob,
+                  const typename Prec<T>::acc *__restrict__ Pg, T *__restrict__ X)
 {
     using Acc = typename Prec<T>::acc;
-    __shared__ Acc Ts[32 * 32];
-    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) Ts[e] = Tglob[e];
+    constexpr int BW = std::is_same<T, double>::value ? 16 : 32;
+    __shared__ Acc Ts[32 * 32], Ls[32 * 32];
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) { Ts[e] = Tglob[e]; Ls[e] = Tglob[32 * 32 + e]; }
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < k; i += gridDim.x * 8) {
-        const Acc a = lane < b ? to_acc<T>(A[(long)i * n + k + lane]) : Acc(0);
-        Acc sacc = Acc(0);
-        for (int t = 0; t < b; t++) sacc = fma(-__shfl_sync(0xffffffffu, a, t), Ts[t * 32 + lane], sacc);
-        if (lane < b) X[(long)i * b + lane] = from_acc<T>(sacc);
+    const int tot = k + (R > b ? R - b : 0);
+    for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < tot; i += gridDim.x * 8) {
+        if (i < k) {
+            const Acc a = lane < b ? to_acc<T>(A[(long)i * n + k + lane]) : Acc(0);
+            Acc sacc = Acc(0);
+            for (int t = 0; t < b; t++) sacc = fma(-__shfl_sync(0xffffffffu, a, t), Ts[t * 32 + lane], sacc);
+            if (lane < b) X[(long)i * b + lane] = from_acc<T>(sacc);
+        } else {
+            const int gi = b + (i - k);
+            const Acc a = lane < b ? Pg[(long)gi * BW + lane] : Acc(0);
+            Acc sacc = Acc(0);
+            for (int t = 0; t < b; t++) sacc = fma(-__shfl_sync(0xffffffffu, a, t), Ls[t * 32 + lane], sacc);
+            if (lane < b) X[(long)(k + gi) * b + lane] = from_acc<T>(sacc);
+        }
     }
 }
 
@@ -862,7 +852,7 @@ static int gje_panel_launch(cudaStream_t s, int n, int k, int b, T *A, GjeWork &
                                                 (Acc *)w.Pglob, use_smem ? 1 : 0);
         return launched();
     }
-    void (*kern)(int, int, int, int, const T *, T *, int *, int *, int *, int *, Acc *);
+    void (*kern)(int, int, int, int, const T *, T *, int *, int *, int *, int *, Acc *, Acc *);
     if (NTh == 1024) kern = (RB > 1024) ? gje_panel_cluster_kernel<T, BW, 2, 1024> : gje_panel_cluster_kernel<T, BW, 1, 1024>;
     else kern = (RB > 512) ? gje_panel_cluster_kernel<T, BW, 2, 512> : gje_panel_cluster_kernel<T, BW, 1, 512>;
     static bool attr = false;
@@ -886,12 +876,12 @@ static int gje_panel_launch(cudaStream_t s, int n, int k, int b, T *A, GjeWork &
     cfg.attrs = at;
     cfg.numAttrs = 1;
     LYAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, n, k, b, RB, (const T *)A, (T *)w.X, w.ipiv, w.moved, w.nmoved,
-                                     w.info, (Acc *)w.Tg));
+                                     w.info, (Acc *)w.Tg, (Acc *)w.Pglob));
     LYAP_TRY(launched());
-    if (k > 0) {
-        gje_xabove_kernel<T><<<std::min(ceil_div(k, 8), 1184), 256, 0, s>>>(n, k, b, (const T *)A, (const Acc *)w.Tg,
-                                                                          (T *)w.X);
-    }
+    const int rows = k + std::max(0, R - b);                 // above the panel + below the block
+    if (rows > 0)
+        gje_xabove_kernel<T><<<std::min(ceil_div(rows, 8), 1184), 256, 0, s>>>(n, k, b, R, (const T *)A, (const Acc *)w.Tg,
+                                                                             (const Acc *)w.Pglob, (T *)w.X);
     return launched();
 }
 
