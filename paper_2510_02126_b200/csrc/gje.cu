@@ -791,36 +791,74 @@ void GjeWork::release() {
     ints = oints = omoved = onmoved = slot_of = invprev = nullptr;
 }
 
-// X rows above the panel: X[i, :] = -A[i, k:k+b] T for i < k.  One warp per row: the
-// row's b panel entries are read once (coalesced) and broadcast by shuffles; same
-// summation order as the single-CTA kernel.
-// Rows below the block (cluster panel): X[k+gi, :] = -P[gi, :] Linv with the multipliers P
-// the panel left in Pg (Acc precision, ld BW) and Linv = Tglob[1024..]; the summation
-// order is the panel's (t ascending from 0).
+// X rows above the panel: X[i, :] = -A[i, k:k+b] T for i < k, and rows below the block
+// (cluster panel): X[k+gi, :] = -P[gi, :] Linv with the multipliers P the panel left in Pg
+// (Acc precision, ld BW) and Linv = Tglob[1024..].  One thread per row: the row's b
+// entries in registers, T / Linv rows as 16-byte shared broadcasts, 16-byte stores; per
+// element the summation order is the panel's (t ascending from 0).
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
 gje_xabove_kernel(int n, int k, int b, int R, const T *__restrict__ A, const typename Prec<T>::acc *__restrict__ Tglob,
                   const typename Prec<T>::acc *__restrict__ Pg, T *__restrict__ X)
 {
     using Acc = typename Prec<T>::acc;
     constexpr int BW = std::is_same<T, double>::value ? 16 : 32;
-    __shared__ Acc Ts[32 * 32], Ls[32 * 32];
-    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) { Ts[e] = Tglob[e]; Ls[e] = Tglob[32 * 32 + e]; }
+    constexpr int VE = Vec16<T>::E;
+    __shared__ __align__(16) Acc TL[2][32 * 32];               // T, Linv
+    for (int e = threadIdx.x; e < 2 * 32 * 32; e += blockDim.x) TL[e >> 10][e & 1023] = Tglob[e];
     __syncthreads();
-    const int lane = threadIdx.x & 31;
     const int tot = k + (R > b ? R - b : 0);
-    for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < tot; i += gridDim.x * 8) {
+    const bool full = (b == BW);
+    const bool vecA = full && ((long)n * sizeof(T)) % 16 == 0 && ((long)k * sizeof(T)) % 16 == 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += gridDim.x * blockDim.x) {
+        Acc a[BW];
+        const Acc *M;
+        T *xr;
         if (i < k) {
-            const Acc a = lane < b ? to_acc<T>(A[(long)i * n + k + lane]) : Acc(0);
-            Acc sacc = Acc(0);
-            for (int t = 0; t < b; t++) sacc = fma(-__shfl_sync(0xffffffffu, a, t), Ts[t * 32 + lane], sacc);
-            if (lane < b) X[(long)i * b + lane] = from_acc<T>(sacc);
+            const T *src = A + (long)i * n + k;
+            if (vecA) {
+#pragma unroll
+                for (int u = 0; u < BW / VE; u++) {
+                    Acc o[VE];
+                    Vec16<T>::unpack(reinterpret_cast<const uint4 *>(src)[u], o);
+#pragma unroll
+                    for (int e = 0; e < VE; e++) a[u * VE + e] = o[e];
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < BW; t++) a[t] = (t < b) ? to_acc<T>(src[t]) : Acc(0);
+            }
+            M = TL[0];
+            xr = X + (long)i * b;
         } else {
             const int gi = b + (i - k);
-            const Acc a = lane < b ? Pg[(long)gi * BW + lane] : Acc(0);
-            Acc sacc = Acc(0);
-            for (int t = 0; t < b; t++) sacc = fma(-__shfl_sync(0xffffffffu, a, t), Ls[t * 32 + lane], sacc);
-            if (lane < b) X[(long)(k + gi) * b + lane] = from_acc<T>(sacc);
+            const Acc *src = Pg + (long)gi * BW;
+#pragma unroll
+            for (int t = 0; t < BW; t++) a[t] = (t < b) ? src[t] : Acc(0);
+            M = TL[1];
+            xr = X + (long)(k + gi) * b;
+        }
+        if (full) {
+#pragma unroll
+            for (int c0 = 0; c0 < BW; c0 += VE) {
+                Acc acc[VE];
+#pragma unroll
+                for (int e = 0; e < VE; e++) acc[e] = Acc(0);
+#pragma unroll
+                for (int t = 0; t < BW; t++) {
+                    const Acc m = -a[t];
+#pragma unroll
+                    for (int e = 0; e < VE; e++) acc[e] = fma(m, M[t * 32 + c0 + e], acc[e]);
+                }
+                reinterpret_cast<uint4 *>(xr)[c0 / VE] = Vec16<T>::pack(acc);
+            }
+        } else {
+            for (int c = 0; c < b; c++) {
+                Acc sacc = Acc(0);
+#pragma unroll
+                for (int t = 0; t < BW; t++) if (t < b) sacc = fma(-a[t], M[t * 32 + c], sacc);
+                xr[c] = from_acc<T>(sacc);
+            }
         }
     }
 }
@@ -880,8 +918,8 @@ static int gje_panel_launch(cudaStream_t s, int n, int k, int b, T *A, GjeWork &
     LYAP_TRY(launched());
     const int rows = k + std::max(0, R - b);                 // above the panel + below the block
     if (rows > 0)
-        gje_xabove_kernel<T><<<std::min(ceil_div(rows, 8), 1184), 256, 0, s>>>(n, k, b, R, (const T *)A, (const Acc *)w.Tg,
-                                                                             (const Acc *)w.Pglob, (T *)w.X);
+        gje_xabove_kernel<T><<<std::min(ceil_div(rows, 128), 1184), 128, 0, s>>>(n, k, b, R, (const T *)A, (const Acc *)w.Tg,
+                                                                               (const Acc *)w.Pglob, (T *)w.X);
     return launched();
 }
 
