@@ -6,7 +6,7 @@
 namespace lyap {
 
 // Workspace of the blocked Gauss-Jordan inversion (gje.cu).
-constexpr int GJE_NB = 256;       // outer block of the two-level Gauss-Jordan scheme (16-bit types)
+constexpr int GJE_NB = 512;        // outer block of the two-level Gauss-Jordan scheme (16-bit types)
 struct GjeWork {
     int n = 0, prec = 0;
     void *X = nullptr, *B = nullptr, *tmp = nullptr, *Pglob = nullptr, *Tg = nullptr, *Bo = nullptr, *tmp2 = nullptr;

@@ -72,11 +72,11 @@ def test_invert_low_precision_bound(gpu, orc, prec, dt, n):
 
 @pytest.mark.parametrize("prec,dt", [("fp16", torch.float16), ("bf16", torch.bfloat16)])
 def test_invert_two_level_ragged(gpu, orc, prec, dt, monkeypatch):
-    """Two-level Gauss-Jordan (outer blocks of 256, ragged last block, look-ahead stream):
+    """Two-level Gauss-Jordan (outer blocks of 512, ragged last block, look-ahead stream):
     within the first-order bound of the exact inverse, as is the one-level sweep, and the
-    two differ only by rounding (the rank-256 update rounds the rest columns once instead
+    two differ only by rounding (the rank-512 update rounds the rest columns once instead
     of after every rank-32 step)."""
-    n = 776                                                  # 256 + 256 + 256 + 8
+    n = 1288                                                 # 512 + 512 + 256 + 8
     rng = np.random.default_rng(776)
     A = rng.standard_normal((n, n)) / np.sqrt(n) + 2 * np.eye(n)
     A = orc.round_(A, prec)
