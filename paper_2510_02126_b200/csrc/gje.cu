@@ -680,11 +680,13 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 gje_outer_scatter_kernel(int n, int K0, int nb, T *__restrict__ A, const int *__restrict__ omoved,
                          const int *__restrict__ onmoved, const T *__restrict__ tmp2, T *__restrict__ Bo,
-                         const int *__restrict__ slot_of)
+                         const int *__restrict__ slot_of, int moved_part)
 {
     const int m = *onmoved;
     const int nrest = n - nb;
-    if (blockIdx.y == 0) {
+    // two launches: moved_part = 0 transposes the pivot rows (grid.y = 1), moved_part = 1
+    // writes moved row blockIdx.y (a narrow grid.x: most of the 2 nb slots are real rows)
+    if (!moved_part) {
         // pivot rows: tile of 32 rest columns x nb rows
         __shared__ T tile[32][33];
         __shared__ int slot[GJE_NB];
@@ -716,7 +718,7 @@ gje_outer_scatter_kernel(int n, int K0, int nb, T *__restrict__ A, const int *__
             }
         }
     } else {
-        const int t = blockIdx.y - 1;
+        const int t = blockIdx.y;
         if (t >= m) return;
         const int dst = omoved[2 * t];
         if (dst < K0 + nb) return;                               // pivot rows handled above
@@ -940,7 +942,11 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
     // look-ahead (two-level only): the inner steps (pivot panels) of block K0+NB run on the
     // high-priority side stream P while the main stream finishes the outer update of block
     // K0; the next block's columns are updated first so P can start early.
-    const bool ahead = two_level && w.side != nullptr && !env_flag("LYAP_GJE_NO_LOOKAHEAD");
+    // Opt-in (LYAP_GJE_LOOKAHEAD=1): with outer blocks of 512 it measured no faster than the
+    // serial order at n = 16384 (74.2 ms either way) and occasionally much slower (one run
+    // in ~12 at 270 ms: the 16-CTA panel cluster cannot always be placed beside the capped
+    // persistent GEMM, so it waits for the whole update).
+    const bool ahead = two_level && w.side != nullptr && env_flag("LYAP_GJE_LOOKAHEAD");
     cudaStream_t P = ahead ? w.side : s;
     if (ahead) {
         LYAP_CUDA_TRY(cudaEventRecord(w.ev_a, s));
@@ -989,12 +995,17 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
             gje_outer_perm2_kernel<<<std::min(ceil_div(n - K0, 256), 592), 256, 0, s>>>(n, K0, nbk, w.rowperm, w.invprev,
                                                                                       w.omoved, w.onmoved, w.slot_of);
             LYAP_TRY(launched());
-            const int gx = std::min(ceil_div(n - nbk, 256), 64);
+            // moved rows: one CTA row per list slot, 8 CTAs across the columns (the grid is
+            // sized for the 2 nb possible slots; unused slots exit at once)
+            const int gx = std::min(ceil_div(n - nbk, 256), 8);
             gje_outer_gather_kernel<T><<<dim3(gx, 2 * nbk), 256, 0, s>>>(n, K0, nbk, A, w.omoved, w.onmoved,
                                                                        (T *)w.tmp2);
             LYAP_TRY(launched());
-            gje_outer_scatter_kernel<T><<<dim3(std::min(ceil_div(n - nbk, 32), 592), 1 + 2 * nbk), 256, 0, s>>>(
-                n, K0, nbk, A, w.omoved, w.onmoved, (const T *)w.tmp2, (T *)w.Bo, w.slot_of);
+            gje_outer_scatter_kernel<T><<<dim3(std::min(ceil_div(n - nbk, 32), 592), 1), 256, 0, s>>>(
+                n, K0, nbk, A, w.omoved, w.onmoved, (const T *)w.tmp2, (T *)w.Bo, w.slot_of, 0);
+            LYAP_TRY(launched());
+            gje_outer_scatter_kernel<T><<<dim3(gx, 2 * nbk), 256, 0, s>>>(
+                n, K0, nbk, A, w.omoved, w.onmoved, (const T *)w.tmp2, (T *)w.Bo, w.slot_of, 1);
             LYAP_TRY(launched());
             KTimer kt(KC_GJE_UPDATE, s);
             // A[:, rest] += X_outer B_outer, X_outer = the block columns (ld n); the next

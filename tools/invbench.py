@@ -8,9 +8,11 @@ dt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[sys.
 for n in ns:
     g = torch.Generator(device="cuda").manual_seed(n)
     A0 = (torch.randn(n, n, device="cuda", generator=g) / n ** 0.5 - 2 * torch.eye(n, device="cuda")).to(dt)
-    A = A0.clone(); G.invert(A); torch.cuda.synchronize()
+    for _ in range(2):                                   # warm-up (clocks ramp from idle)
+        A = A0.clone(); G.invert(A)
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 3
+    reps = 5
     e0.record()
     for _ in range(reps):
         A.copy_(A0); G.invert(A)
