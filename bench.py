@@ -218,7 +218,7 @@ def run_gpu(args):
     # chosen among the single-kernel classes
     shares = {}
     for name in ["dgemm", "tc_gemm", "qr_panel", "tridiag", "gje_panel", "eig", "qr", "zside_gemm",
-                 "gje_update", "resid_gemm"]:
+                 "gje_update", "resid_gemm", "newton_update"]:
         G.kernel_timing(name)
         solve()
         shares[name] = G.kernel_stats()
@@ -330,6 +330,27 @@ def run_gpu(args):
     roofline = roof(dom, dom_ms, dom_cnt, dom_flops, dom_bytes)
     roofline["measured_over"] = f"a second timed pass of the same {args.steps} solves (events per launch)"
     roofline_sign_newton = roof("tc_gemm", *tcs) if tcs[1] > 0 else None
+    # the residual factor's A Z (fp64, Fragments 1/3): its fp64 tensor rate and the HBM rate of
+    # its algorithmic bytes (A once, Z in, A Z out); at the ranks configs[1] reaches
+    # (c ~ 420) it is a contraction with ~50 flop/byte, i.e. tensor-, not HBM-bound
+    rg_ms, rg_cnt, rg_fl, rg_by = shares["resid_gemm"]
+    roofline_residual = None
+    if rg_cnt > 0 and rg_ms > 0:
+        roofline_residual = roof("dgemm", rg_ms, rg_cnt, rg_fl, rg_by)
+        roofline_residual["kernel"] = "resid_gemm (A Z, fp64 DMMA)"
+        roofline_residual["traffic"] = traffic_all.get("resid_gemm")
+        roofline_residual["hbm_gbs_algorithmic"] = rg_by / (rg_ms / 1e3) / 1e9
+        roofline_residual["hbm_frac"] = roofline_residual["hbm_gbs_algorithmic"] / pk["hbm"]
+        roofline_residual["measured_over"] = "one untimed solve (events per launch)"
+    nu_ms, nu_cnt, _, nu_by = shares["newton_update"]
+    roofline_newton_update = None
+    if nu_cnt > 0 and nu_ms > 0:
+        g = nu_by / (nu_ms / 1e3) / 1e9
+        roofline_newton_update = {"kernel": "newton_update", "bound": "hbm", "achieved": g, "peak": pk["hbm"],
+                                  "unit": "GB/s", "frac": g / pk["hbm"], "launches_timed": nu_cnt,
+                                  "algorithmic_per_launch": nu_by / nu_cnt,
+                                  "avg_launch_us": nu_ms / nu_cnt * 1e3, "traffic": None,
+                                  "measured_over": "one untimed solve (events per launch)"}
     newton_tflops = rep["newton_flops"] / (rep["newton_ms"] / 1e3) / 1e12 if rep["newton_ms"] > 0 else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -345,6 +366,7 @@ def run_gpu(args):
         "phase_ms": {"newton": rep["newton_ms"], "residual": rep["residual_ms"], "update": rep["update_ms"]},
         "sign_newton_tflops": newton_tflops,
         "sign_newton_frac_of_fp16_peak": (newton_tflops / pk["bf16"]) if newton_tflops else None,
+        "roofline_residual": roofline_residual, "roofline_newton_update": roofline_newton_update,
         "kernel_class_ms_one_solve": {k: round(v[0], 4) for k, v in shares.items()},
         "roofline": roofline,
         "roofline_sign_newton_tc_gemm": roofline_sign_newton,
@@ -403,6 +425,19 @@ def sign_newton_scale(G, P, dev, pk, which):
     res["tc_gemm"] = {"bound": "tensor", "achieved": ach, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
                       "frac": ach / pk["bf16_sus"], "launches": cnt, "ms": ms_t}
     res["class_ms"] = {k2: v[0] for k2, v in classes.items()}
+    # the fused Newton averaging update (HBM-streaming: read A_k and the inverse, write
+    # A_{k+1} and the cached A_k^{-1}: 4 x 2 n^2 bytes per launch in fp16)
+    G.kernel_timing("newton_update")
+    s.newton_aseq(A)
+    ms_u, cnt_u, _, by_u = G.kernel_stats()
+    G.kernel_timing(None)
+    gbs = by_u / (ms_u / 1e3) / 1e9 if ms_u > 0 else 0.0
+    res["newton_update"] = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm"], "unit": "GB/s",
+                            "frac": gbs / pk["hbm"], "launches": cnt_u, "ms": ms_u,
+                            "algorithmic_bytes_per_launch": by_u / max(cnt_u, 1)}
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if which == "cfg3" and os.path.exists(tf):
+        res["newton_update"]["traffic"] = json.load(open(tf)).get("newton_update_n16384")
     del s, A
     torch.cuda.empty_cache()
     return res

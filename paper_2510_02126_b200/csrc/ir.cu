@@ -271,7 +271,7 @@ int build_F(lyap_ir_ctx *h, const double *A, const double *L, int m, int c, cons
     cudaStream_t s = h->s;
     LYAP_TRY(nk_copy_block(s, n, c, Z, n, h->F, n, 1.0));
     {
-        KTimer kt(KC_RESID_GEMM, s);
+        KTimer kt(KC_RESID_GEMM, s, 2.0 * n * (double)n * c, 8.0 * ((double)n * n + 2.0 * n * c));
         LYAP_TRY(gemm_strided<double, double, double, double>(s, n, c, n, 1.0, A, n, 1, Z, 1, n, 0.0,
                                                               h->F + (size_t)n * c, 1, n));
     }

@@ -15,6 +15,7 @@
 #include "common.cuh"
 #include "lyap_internal.h"
 #include "newton_kernels.h"
+#include "ktimer.h"
 
 namespace lyap {
 
@@ -34,6 +35,38 @@ cast_kernel(int n, const double *__restrict__ A, T *__restrict__ Ak, double *__r
             double d = to_d<T>(v);
             ss = fma(d, d, ss);
             mx = fmax(mx, fabs(d));
+        }
+        ss = block_sum(ss, red);
+        mx = block_max(mx, red);
+        if (threadIdx.x == 0) { part[4 * i + 0] = 0.0; part[4 * i + 1] = ss; part[4 * i + 2] = 0.0; part[4 * i + 3] = mx; }
+    }
+}
+
+// Same cast on row vectors: 16 bytes of A_k written per thread per pass, the fp64 source
+// read as double2 (n a multiple of 16 / sizeof(T)).
+template <typename T>
+__global__ void __launch_bounds__(256)
+cast_vec_kernel(int n, const double *__restrict__ A, T *__restrict__ Ak, double *__restrict__ part)
+{
+    __shared__ double red[32];
+    constexpr int V = 16 / sizeof(T);
+    const int nv = n / V;
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const double2 *Ai = reinterpret_cast<const double2 *>(A + (long)i * n);
+        uint4 *Oi = reinterpret_cast<uint4 *>(Ak + (long)i * n);
+        double ss = 0.0, mx = 0.0;
+        for (int j = threadIdx.x; j < nv; j += blockDim.x) {
+            uint4 w;
+            T *o = reinterpret_cast<T *>(&w);
+#pragma unroll
+            for (int t = 0; t < V / 2; t++) {
+                const double2 a = __ldcs(Ai + (long)j * (V / 2) + t);
+                o[2 * t] = from_d<T>(a.x);
+                o[2 * t + 1] = from_d<T>(a.y);
+            }
+#pragma unroll
+            for (int t = 0; t < V; t++) { const double d = to_d<T>(o[t]); ss = fma(d, d, ss); mx = fmax(mx, fabs(d)); }
+            Oi[j] = w;
         }
         ss = block_sum(ss, red);
         mx = block_max(mx, red);
@@ -71,6 +104,31 @@ __global__ void scale_kernel(long nn, const T *__restrict__ Ak, T *__restrict__ 
     }
 }
 
+// Same scaling on 16-byte vectors (nn a multiple of 16 / sizeof(T)); exact, so bitwise
+// equal to scale_kernel.
+template <typename T>
+__global__ void __launch_bounds__(256)
+scale_vec_kernel(long nv, const uint4 *__restrict__ Ak, uint4 *__restrict__ W, double *__restrict__ scal)
+{
+    constexpr int V = 16 / sizeof(T);
+    int e;
+    frexp(scal[SC_MAXA], &e);
+    if (scal[SC_MAXA] == 0.0) e = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) scal[SC_EXP] = (double)e;
+    const float f = ldexpf(1.0f, -e);
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < nv; idx += (long)gridDim.x * blockDim.x) {
+        uint4 v = __ldcs(Ak + idx), w;
+        const T *a = reinterpret_cast<const T *>(&v);
+        T *o = reinterpret_cast<T *>(&w);
+#pragma unroll
+        for (int t = 0; t < V; t++) {
+            if constexpr (sizeof(T) == 8) o[t] = ldexp(to_d<T>(a[t]), -e);
+            else o[t] = from_f<T>(to_f<T>(a[t]) * f);
+        }
+        W[idx] = w;
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256)
 sumsq_rows_kernel(int n, const T *__restrict__ G, double *__restrict__ part)
@@ -79,6 +137,28 @@ sumsq_rows_kernel(int n, const T *__restrict__ G, double *__restrict__ part)
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
         double ss = 0.0;
         for (int j = threadIdx.x; j < n; j += blockDim.x) { double d = to_d<T>(G[(long)i * n + j]); ss = fma(d, d, ss); }
+        ss = block_sum(ss, red);
+        if (threadIdx.x == 0) { part[4 * i] = ss; part[4 * i + 1] = 0.0; part[4 * i + 2] = 0.0; part[4 * i + 3] = 0.0; }
+    }
+}
+
+// Same partials from 16-byte row vectors (n a multiple of 16 / sizeof(T)).
+template <typename T>
+__global__ void __launch_bounds__(256)
+sumsq_rows_vec_kernel(int n, const T *__restrict__ G, double *__restrict__ part)
+{
+    __shared__ double red[32];
+    constexpr int V = 16 / sizeof(T);
+    const int nv = n / V;
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const uint4 *Gi = reinterpret_cast<const uint4 *>(G + (long)i * n);
+        double ss = 0.0;
+        for (int j = threadIdx.x; j < nv; j += blockDim.x) {
+            uint4 v = Gi[j];
+            const T *g = reinterpret_cast<const T *>(&v);
+#pragma unroll
+            for (int t = 0; t < V; t++) { double d = to_d<T>(g[t]); ss = fma(d, d, ss); }
+        }
         ss = block_sum(ss, red);
         if (threadIdx.x == 0) { part[4 * i] = ss; part[4 * i + 1] = 0.0; part[4 * i + 2] = 0.0; part[4 * i + 3] = 0.0; }
     }
@@ -128,6 +208,68 @@ newton_update_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ G, c
         }
         dd = block_sum(dd, red); ss = block_sum(ss, red);
         rs = block_sum(rs, red); mx = block_max(mx, red);
+        if (threadIdx.x == 0) { part[4 * i] = dd; part[4 * i + 1] = ss; part[4 * i + 2] = rs; part[4 * i + 3] = mx; }
+    }
+}
+
+// The same update, HBM-streaming form: row i of G (the column-permuted inverse) is staged
+// in shared memory with 16-byte loads, so the invperm gather hits shared memory instead of
+// scattered 32-byte sectors; A_k is read and A_{k+1}, A_k^{-1} are written as 16-byte
+// vectors (V = 16 / sizeof(T) elements per thread per pass).  Per-element arithmetic is
+// the kernel's above; only the order of the fp64 row partials differs.  Algorithmic
+// traffic per row: read A_k, G (2 n sizeof(T)), write A_{k+1}, A_k^{-1} (2 n sizeof(T)).
+// (A cp.async double-buffered G row measured slower: 2.5 vs 3.2 TB/s at n = 16384, the
+// second buffer costing a resident CTA per SM.)
+template <typename T>
+__global__ void __launch_bounds__(256, 5)
+newton_update_row_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ G, const int *__restrict__ invperm,
+                         T *__restrict__ Anext, T *__restrict__ Ainv, const double *__restrict__ scal,
+                         double *__restrict__ part)
+{
+    extern __shared__ __align__(16) unsigned char nu_smem[];
+    T *g = reinterpret_cast<T *>(nu_smem);
+    __shared__ double red[32];
+    constexpr int V = 16 / sizeof(T);
+    using Acc = typename Prec<T>::acc;
+    const double mu = scal[SC_MU];
+    const int e = (int)scal[SC_EXP];
+    const Acc a = (Acc)mu, b = (Acc)(1.0 / mu);
+    const int nv = n / V;                       // caller guarantees n % V == 0
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const uint4 *Gi = reinterpret_cast<const uint4 *>(G + (long)i * n);
+        for (int j = threadIdx.x; j < nv; j += blockDim.x) reinterpret_cast<uint4 *>(g)[j] = __ldcs(Gi + j);
+        __syncthreads();
+        const uint4 *Ai = reinterpret_cast<const uint4 *>(Ak + (long)i * n);
+        uint4 *Ni = reinterpret_cast<uint4 *>(Anext + (long)i * n);
+        uint4 *Ii = reinterpret_cast<uint4 *>(Ainv + (long)i * n);
+        double dd = 0.0, ss = 0.0, rs = 0.0, mx = 0.0;
+        for (int jv = threadIdx.x; jv < nv; jv += blockDim.x) {
+            uint4 av = __ldcs(Ai + jv), iv, nw;
+            const T *ae = reinterpret_cast<const T *>(&av);
+            T *ie = reinterpret_cast<T *>(&iv), *ne = reinterpret_cast<T *>(&nw);
+#pragma unroll
+            for (int t = 0; t < V; t++) {
+                const int j = jv * V + t;
+                T gi;
+                if constexpr (sizeof(T) == 8) gi = ldexp(g[invperm[j]], -e);
+                else gi = from_f<T>(ldexpf(to_f<T>(g[invperm[j]]), -e));
+                ie[t] = gi;
+                Acc x = to_acc<T>(ae[t]);
+                Acc y = to_acc<T>(gi);
+                T nvt = from_acc<T>(Acc(0.5) * fma(a, x, b * y));
+                ne[t] = nvt;
+                double nd = to_d<T>(nvt), xd = (double)x;
+                dd = fma(nd - xd, nd - xd, dd);
+                ss = fma(nd, nd, ss);
+                rs += fabs(nd + (i == j ? 1.0 : 0.0));
+                mx = fmax(mx, fabs(nd));
+                if (!isfinite(nd)) mx = INFINITY;
+            }
+            Ii[jv] = iv;
+            Ni[jv] = nw;
+        }
+        dd = block_sum(dd, red); ss = block_sum(ss, red);     // block_sum's barriers also
+        rs = block_sum(rs, red); mx = block_max(mx, red);     // free g for the next row
         if (threadIdx.x == 0) { part[4 * i] = dd; part[4 * i + 1] = ss; part[4 * i + 2] = rs; part[4 * i + 3] = mx; }
     }
 }
@@ -380,7 +522,14 @@ static inline int grid_for(long n, int bs = 256, int cap = 4096) { int g = ceil_
     }
 
 template <typename T> static void k_cast(cudaStream_t s, int n, const double *A, void *Ak, double *part)
-{ cast_kernel<T><<<n < 4096 ? n : 4096, 256, 0, s>>>(n, A, (T *)Ak, part); }
+{
+    // caller-owned A: the vector form needs 16-byte aligned rows
+    if (n % (16 / (int)sizeof(T)) == 0 && reinterpret_cast<uintptr_t>(A) % 16 == 0) {
+        cast_vec_kernel<T><<<n < 148 * 8 ? n : 148 * 8, 256, 0, s>>>(n, A, (T *)Ak, part);
+        return;
+    }
+    cast_kernel<T><<<n < 4096 ? n : 4096, 256, 0, s>>>(n, A, (T *)Ak, part);
+}
 int nk_cast(cudaStream_t s, int prec, int n, const double *A, void *Ak, double *part, double *out)
 {
     DISPATCH_T(prec, k_cast, s, n, A, Ak, part);
@@ -390,7 +539,14 @@ int nk_cast(cudaStream_t s, int prec, int n, const double *A, void *Ak, double *
 }
 
 template <typename T> static void k_scale(cudaStream_t s, long nn, const void *Ak, void *W, double *scal)
-{ scale_kernel<T><<<grid_for(nn), 256, 0, s>>>(nn, (const T *)Ak, (T *)W, scal); }
+{
+    constexpr int V = 16 / sizeof(T);
+    if (nn % V == 0) {
+        scale_vec_kernel<T><<<grid_for(nn / V, 256, 148 * 8), 256, 0, s>>>(nn / V, (const uint4 *)Ak, (uint4 *)W, scal);
+        return;
+    }
+    scale_kernel<T><<<grid_for(nn), 256, 0, s>>>(nn, (const T *)Ak, (T *)W, scal);
+}
 int nk_scale(cudaStream_t s, int prec, long nn, const void *Ak, void *W, double *scal)
 {
     DISPATCH_T(prec, k_scale, s, nn, Ak, W, scal);
@@ -398,7 +554,13 @@ int nk_scale(cudaStream_t s, int prec, long nn, const void *Ak, void *W, double 
 }
 
 template <typename T> static void k_sumsq(cudaStream_t s, int n, const void *G, double *part)
-{ sumsq_rows_kernel<T><<<n < 4096 ? n : 4096, 256, 0, s>>>(n, (const T *)G, part); }
+{
+    if (n % (16 / (int)sizeof(T)) == 0) {
+        sumsq_rows_vec_kernel<T><<<n < 148 * 8 ? n : 148 * 8, 256, 0, s>>>(n, (const T *)G, part);
+        return;
+    }
+    sumsq_rows_kernel<T><<<n < 4096 ? n : 4096, 256, 0, s>>>(n, (const T *)G, part);
+}
 int nk_mu(cudaStream_t s, int prec, int n, const void *G, double *part, double *scal, int scaling)
 {
     DISPATCH_T(prec, k_sumsq, s, n, G, part);
@@ -409,13 +571,40 @@ int nk_mu(cudaStream_t s, int prec, int n, const void *G, double *part, double *
     return launched();
 }
 
+// Row-staged form when a row of G fits the shared-memory budget and rows are 16-byte
+// multiples; grid = resident CTAs per SM x SMs (rows are grid-strided).
+static constexpr int NU_SMEM_MAX = 96 * 1024;
 template <typename T> static void k_update(cudaStream_t s, int n, const void *Ak, const void *G, const int *ip,
                                            void *An, void *Ai, const double *scal, double *part)
-{ newton_update_kernel<T><<<n < 4096 ? n : 4096, 256, 0, s>>>(n, (const T *)Ak, (const T *)G, ip, (T *)An, (T *)Ai, scal, part); }
+{
+    const size_t smem = (size_t)n * sizeof(T);
+    if (n % (16 / (int)sizeof(T)) == 0 && smem <= (size_t)NU_SMEM_MAX) {
+        static const int nsm = [] {
+            cudaFuncSetAttribute(newton_update_row_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, NU_SMEM_MAX);
+            cudaFuncSetAttribute(newton_update_row_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            int dev = 0, v = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+            return v;
+        }();
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, newton_update_row_kernel<T>, 256, smem);
+        if (per_sm < 1) per_sm = 1;
+        const int grid = n < nsm * per_sm ? n : nsm * per_sm;
+        newton_update_row_kernel<T><<<grid, 256, smem, s>>>(n, (const T *)Ak, (const T *)G, ip, (T *)An, (T *)Ai,
+                                                             scal, part);
+        return;
+    }
+    newton_update_kernel<T><<<n < 4096 ? n : 4096, 256, 0, s>>>(n, (const T *)Ak, (const T *)G, ip, (T *)An, (T *)Ai, scal, part);
+}
 int nk_update(cudaStream_t s, int prec, int n, const void *Ak, const void *G, const int *invperm, void *Anext,
               void *Ainv, double *scal, double *part)
 {
-    DISPATCH_T(prec, k_update, s, n, Ak, G, invperm, Anext, Ainv, scal, part);
+    {
+        const double es = prec == LYAP_FP64 ? 8.0 : prec == LYAP_FP32 ? 4.0 : 2.0;
+        KTimer kt(KC_NEWTON_UPDATE, s, 0.0, 4.0 * es * (double)n * n);
+        DISPATCH_T(prec, k_update, s, n, Ak, G, invperm, Anext, Ainv, scal, part);
+    }
     LYAP_TRY(launched());
     reduce_rows_kernel<<<1, 1024, 0, s>>>(n, part, scal + SC_RED);
     return launched();

@@ -206,10 +206,13 @@ def test_rank_trunc_ldlt_parity(gpu, orc):
 
 # ------------------------------------------------------------------ Newton
 @pytest.mark.parametrize("us", ["fp64", "fp32", "fp16", "bf16"])
-def test_newton_aseq_counts(gpu, orc, us):
-    """The A-side step count (an integer decided by floats) matches the oracle's."""
-    p = P.paper_synthetic(100, 3, 1.0, seed=0)
-    s = gpu.Solver(100, us=us, max_cols=64)
+@pytest.mark.parametrize("n", [100, 128])
+def test_newton_aseq_counts(gpu, orc, us, n):
+    """The A-side step count (an integer decided by floats) matches the oracle's.  n = 128
+    takes the row-staged 16-byte Newton update in every precision, n = 100 the element-wise
+    one for fp16/bf16."""
+    p = P.paper_synthetic(n, 3, 1.0, seed=0)
+    s = gpu.Solver(n, us=us, max_cols=64)
     out = s.newton_aseq(cuda(p.A))
     q = orc.aseq(us, p.A)
     assert out["steps"] == q.steps
