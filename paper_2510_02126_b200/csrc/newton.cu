@@ -218,10 +218,11 @@ newton_update_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ G, c
 // vectors (V = 16 / sizeof(T) elements per thread per pass).  Per-element arithmetic is
 // the kernel's above; only the order of the fp64 row partials differs.  Algorithmic
 // traffic per row: read A_k, G (2 n sizeof(T)), write A_{k+1}, A_k^{-1} (2 n sizeof(T)).
-// (A cp.async double-buffered G row measured slower: 2.5 vs 3.2 TB/s at n = 16384, the
-// second buffer costing a resident CTA per SM.)
+// (Measured slower at n = 16384: a cp.async double-buffered G row, 2.5 vs 3.2 TB/s, the
+// second buffer costing a resident CTA per SM; __launch_bounds__(256, 5), 810 vs 673 us,
+// register spills; a 100 % shared-memory carveout, 2.75 TB/s: the invperm reads lose L1.)
 template <typename T>
-__global__ void __launch_bounds__(256, 5)
+__global__ void __launch_bounds__(256)
 newton_update_row_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ G, const int *__restrict__ invperm,
                          T *__restrict__ Anext, T *__restrict__ Ainv, const double *__restrict__ scal,
                          double *__restrict__ part)
@@ -581,7 +582,6 @@ template <typename T> static void k_update(cudaStream_t s, int n, const void *Ak
     if (n % (16 / (int)sizeof(T)) == 0 && smem <= (size_t)NU_SMEM_MAX) {
         static const int nsm = [] {
             cudaFuncSetAttribute(newton_update_row_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, NU_SMEM_MAX);
-            cudaFuncSetAttribute(newton_update_row_kernel<T>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
             int dev = 0, v = 148;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
