@@ -220,7 +220,9 @@ newton_update_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ G, c
 // traffic per row: read A_k, G (2 n sizeof(T)), write A_{k+1}, A_k^{-1} (2 n sizeof(T)).
 // (Measured slower at n = 16384: a cp.async double-buffered G row, 2.5 vs 3.2 TB/s, the
 // second buffer costing a resident CTA per SM; __launch_bounds__(256, 5), 810 vs 673 us,
-// register spills; a 100 % shared-memory carveout, 2.75 TB/s: the invperm reads lose L1.)
+// register spills; a 100 % shared-memory carveout, 2.75 TB/s: the invperm reads lose L1;
+// invperm staged once per CTA as 16-bit indices in shared memory, 3.0 vs 3.2 TB/s: the
+// extra 32 KB costs a resident CTA.)
 template <typename T>
 __global__ void __launch_bounds__(256)
 newton_update_row_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ G, const int *__restrict__ invperm,
