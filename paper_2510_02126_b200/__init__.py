@@ -131,8 +131,23 @@ def _ptr(t) -> int | None:
     if t is None:
         return None
     import torch
-    assert isinstance(t, torch.Tensor) and t.is_cuda and t.is_contiguous(), "expected contiguous CUDA tensor"
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.is_contiguous()):
+        raise LyapError("expected a contiguous CUDA tensor")
     return t.data_ptr()
+
+
+def _check_f64(name, t, shape, device=None):
+    """Shape / dtype / device check of a solve argument (the C ABI reads exactly this
+    many elements: a smaller or mistyped buffer would be read past its end)."""
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.is_contiguous()):
+        raise LyapError(f"{name}: expected a contiguous CUDA tensor")
+    if t.dtype != torch.float64:
+        raise LyapError(f"{name}: expected float64, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise LyapError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    if device is not None and t.device != device:
+        raise LyapError(f"{name}: on {t.device}, expected {device}")
 
 
 def _stream():
@@ -203,7 +218,11 @@ class Solver:
         """A: (n,n) fp64 CUDA; Lt: (m,n) fp64 CUDA (= L^T); S: (m,m) fp64 CUDA or None."""
         import torch
         n, cm = self.n, self.max_cols
-        m = Lt.shape[0]
+        m = Lt.shape[0] if isinstance(Lt, torch.Tensor) and Lt.dim() == 2 else -1
+        _check_f64("A", A, (n, n))
+        _check_f64("Lt", Lt, (m, n), A.device)
+        if S is not None:
+            _check_f64("S", S, (m, m), A.device)
         if out is None:
             Zt = torch.empty((cm, n), dtype=torch.float64, device=A.device)
             Yb = torch.zeros((cm, cm), dtype=torch.float64, device=A.device) if S is not None else None
@@ -224,6 +243,10 @@ class Solver:
         A = np.ascontiguousarray(A, dtype=np.float64)
         Lt = np.ascontiguousarray(Lt, dtype=np.float64)
         S = None if S is None else np.ascontiguousarray(S, dtype=np.float64)
+        m = Lt.shape[0] if Lt.ndim == 2 else -1
+        if A.shape != (n, n) or Lt.ndim != 2 or Lt.shape[1] != n or (S is not None and S.shape != (m, m)):
+            raise LyapError(f"solve_host: expected A ({n},{n}), Lt (m,{n}), S (m,m); got "
+                            f"{A.shape}, {Lt.shape}, {None if S is None else S.shape}")
         Zt = np.empty((cm, n), dtype=np.float64)
         Yb = np.zeros((cm, cm), dtype=np.float64) if S is not None else None
         rank = C.c_int(0)

@@ -883,11 +883,12 @@ static int gje_panel_launch(cudaStream_t s, int n, int k, int b, T *A, GjeWork &
     if (RB > 2 * NTh || b > BW || env_flag("LYAP_GJE_1CTA")) {
         bool use_smem;
         size_t sm = gje_panel_smem(n, Prec<T>::code, b, R, &use_smem);
-        static bool attr1 = false;
-        if (!attr1) {
-            LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-            attr1 = true;
-        }
+        // one-time setup (function-local static: thread-safe initialisation)
+        static const bool attr1 = [] {
+            cudaFuncSetAttribute(gje_panel_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            return true;
+        }();
+        (void)attr1;
         gje_panel_kernel<T><<<1, 1024, sm, s>>>(n, k, b, A, (T *)w.X, w.ipiv, w.moved, w.nmoved, w.info,
                                                 (Acc *)w.Pglob, use_smem ? 1 : 0);
         return launched();
@@ -895,14 +896,15 @@ static int gje_panel_launch(cudaStream_t s, int n, int k, int b, T *A, GjeWork &
     void (*kern)(int, int, int, int, const T *, T *, int *, int *, int *, int *, Acc *, Acc *);
     if (NTh == 1024) kern = (RB > 1024) ? gje_panel_cluster_kernel<T, BW, 2, 1024> : gje_panel_cluster_kernel<T, BW, 1, 1024>;
     else kern = (RB > 512) ? gje_panel_cluster_kernel<T, BW, 2, 512> : gje_panel_cluster_kernel<T, BW, 1, 512>;
-    static bool attr = false;
-    if (!attr) {
-        LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 1, 1024>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 2, 1024>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 1, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        LYAP_CUDA_TRY(cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 2, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr = true;
-    }
+    // one-time setup (function-local static: thread-safe initialisation)
+    static const bool attr = [] {
+        cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 1, 1024>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 2, 1024>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 1, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(gje_panel_cluster_kernel<T, BW, 2, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        return true;
+    }();
+    (void)attr;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nc, 1, 1);
     cfg.blockDim = dim3(NTh, 1, 1);

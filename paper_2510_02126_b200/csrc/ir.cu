@@ -483,6 +483,7 @@ int ir_solve(lyap_ir_ctx *h, const double *A, const double *L, int m, const doub
     }
     const double nA = std::sqrt(nA2), nW = std::sqrt(std::max(nW2, 0.0));
     int stagn = 0;
+    double prev_rel = 0.0;     // previous relative residual (theta_i, Eq. it-early-terminate l.1413)
     R.status = LYAP_STATUS_MAXSTEPS;
     for (int i = 1;; i++) {
         LYAP_CUDA_TRY(cudaEventRecord(h->ev[2], s));
@@ -503,10 +504,11 @@ int ir_solve(lyap_ir_ctx *h, const double *A, const double *L, int m, const doub
         bool stop = false;
         if (rel <= tol) { R.status = LYAP_STATUS_CONVERGED; stop = true; }
         else if (i >= 2) {
-            double theta = rel / R.res[std::min(R.nres, LYAP_MAX_REPORT) - 2];
+            double theta = rel / prev_rel;
             stagn = (theta > 0.9) ? stagn + 1 : 0;
             if (stagn >= 2) { R.status = LYAP_STATUS_STAGNATED; stop = true; }
         }
+        prev_rel = rel;
         if (!stop && i > maxit) { R.status = LYAP_STATUS_MAXSTEPS; stop = true; }
         if (stop) break;
         // ---- correction equation(s) at u_s (cached A-sequence)

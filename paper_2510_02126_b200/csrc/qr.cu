@@ -610,12 +610,13 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
     const int k = m < n ? m : n;
     double *Wm = w.Wk;
     double *diag = w.tau + k;
-    static bool attr = false;
-    if (!attr) {
+    // one-time setup (function-local static: thread-safe initialisation)
+    static const bool attr = [] {
         cudaFuncSetAttribute(qr_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(qr_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     LYAP_CUDA_TRY(cudaMemcpyAsync(Wm, A, sizeof(double) * (size_t)m * n, cudaMemcpyDeviceToDevice, s));
     // cluster panels (32 wide) while a CTA's row slice fits in shared memory; otherwise
     // the one-CTA panel with widths 32, or 16/8 while the panel would not fit
@@ -634,11 +635,12 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
         if (m - j0 <= 16 * QRT && !env_flag("LYAP_QR_SMEM")) {
             const int nc = ceil_div(m - j0, QRT);
             KTimer kp(KC_QR_PANEL, s, 4.0 * (m - j0) * jb * jb, 16.0 * (m - j0) * jb);
-            static bool attr_r = false;
-            if (!attr_r) {
-                LYAP_CUDA_TRY(cudaFuncSetAttribute(qr_panel_reg_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-                attr_r = true;
-            }
+            // one-time setup (function-local static: thread-safe initialisation)
+            static const bool attr_r = [] {
+                cudaFuncSetAttribute(qr_panel_reg_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                return true;
+            }();
+            (void)attr_r;
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(nc, 1, 1);
             cfg.blockDim = dim3(QRT, 1, 1);

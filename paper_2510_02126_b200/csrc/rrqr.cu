@@ -413,19 +413,23 @@ int rank_trunc_chol_f64(cudaStream_t s, int n, int c, const double *Z, double to
     transpose_init_kernel<<<ceil_div(tot, 256) < 2048 ? ceil_div(tot, 256) : 2048, 256, 0, s>>>(n, c, Z, w.M, perm);
     LYAP_TRY(launched());
     const bool v2 = !env_flag("LYAP_RRQR_V1");
-    static int max_blocks = 0, nsm = 0;
-    if (max_blocks == 0) {
-        int dev, per;
+    // one-time setup (function-local static: thread-safe initialisation, published after
+    // every attribute is set)
+    struct Cfg { int max_blocks, nsm; };
+    static const Cfg cfg = [] {
+        int dev = 0, per = 0, nsm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr_kernel, 256, 0);
-        max_blocks = nsm * (per < 2 ? per : 2);
-        if (max_blocks > 1024) max_blocks = 1024;
-        if (max_blocks < 1) max_blocks = 1;
+        int mb = nsm * (per < 2 ? per : 2);
+        if (mb > 1024) mb = 1024;
+        if (mb < 1) mb = 1;
         for (void *f : {(void *)rrqr2_kernel<0>, (void *)rrqr2_kernel<16>, (void *)rrqr2_kernel<32>,
                         (void *)rrqr2_kernel<48>})
             cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    }
+        return Cfg{mb, nsm};
+    }();
+    const int max_blocks = cfg.max_blocks, nsm = cfg.nsm;
     const int want = ceil_div(n, 8);
     const size_t smem2 = sizeof(double) * (size_t)c;
     // register-resident columns (one load and one store per element, all loads of a column in

@@ -1020,32 +1020,27 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
     symmetrize_copy_kernel<<<gsz, 256, 0, s>>>(p, Ain, W.A);
     LYAP_TRY(launched());
     {
-        static int max_blocks = 0;
-        const size_t smem = sizeof(double) * 4 * (size_t)W.pmax;
+        // shared memory for this p (the kernels address 4 p doubles), not the capacity
+        const size_t smem = sizeof(double) * 4 * (size_t)p;
         if (smem > 200 * 1024) return LYAP_ERR_CAPACITY;
-        if (max_blocks == 0) {
-            int dev, nsm, per = 0;
+        // one-time attribute setup (function-local static: thread-safe initialisation)
+        static const int nsm_t = [] {
+            int dev = 0, v = 0;
             cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
             cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tridiag_kernel, 256, smem);
-            max_blocks = nsm * std::max(1, std::min(per, 1));
-        }
+            for (void *f : {(void *)tridiag_reg_kernel<8>, (void *)tridiag_reg_kernel<16>, (void *)tridiag_reg_kernel<32>,
+                            (void *)tridiag_w_kernel<8, 1>, (void *)tridiag_w_kernel<16, 1>,
+                            (void *)tridiag_w_kernel<32, 1>})
+                cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            return v;
+        }();
+        const int max_blocks = nsm_t;                 // one CTA per SM for the register-resident kernels
         TridArgs ta{p, W.A, W.R, d, e, tau, P};
         void *args[] = {&ta};
         const int need = ceil_div(p, 8);             // one warp per column
         KTimer kt(KC_TRIDIAG, s, (4.0 / 3.0) * (double)p * p * p, 8.0 * (double)p * p);
         if (p >= 3 && p <= 1024 && need <= max_blocks) {
-            static bool attr2 = false;
-            if (!attr2) {
-                cudaFuncSetAttribute(tridiag_reg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                cudaFuncSetAttribute(tridiag_reg_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                cudaFuncSetAttribute(tridiag_reg_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                cudaFuncSetAttribute(tridiag_w_kernel<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                cudaFuncSetAttribute(tridiag_w_kernel<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                cudaFuncSetAttribute(tridiag_w_kernel<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                attr2 = true;
-            }
             void *fn;
             int grid_t = need;
             if (env_flag("LYAP_TRIDIAG_REG")) {
@@ -1103,11 +1098,12 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
             for (auto &x : hm) maxn0 = std::max(maxn0, x.hi - x.lo);
             const size_t msm = 56 * (size_t)maxn0;           // D, z, rot (4n), Dpos, Kpos
             const int use = msm <= 200 * 1024 ? 1 : 0;
-            static bool attr_m = false;
-            if (!attr_m) {
+            // one-time setup (function-local static: thread-safe initialisation)
+            static const bool attr_m = [] {
                 cudaFuncSetAttribute(dc_merge_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                attr_m = true;
-            }
+                return true;
+            }();
+            (void)attr_m;
             dc_merge_prep_kernel<<<nm, 1024, use ? msm : 0, s>>>(p, mi, e, lam, W.Q, perm, Ds, zs, DK, zK, Kpos, Dpos,
                                                                  W.rot, counts, rho, use);
         }

@@ -460,21 +460,19 @@ int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const vo
     dim3 grid(ceil_div(N, tc::BN), ceil_div(M, tc::BM));
     const int ns = tc::stages_for(ceil_div(K, tc::BK));
     const int smem = tc::smem_bytes(ns);
-    static bool attr = false;
-    if (!attr) {
+    // one-time attribute setup; a function-local static is initialised thread-safely, and
+    // nsm is published only after every attribute is set (concurrent solver handles)
+    static const int nsm = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(tc_gemm_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM);
         cudaFuncSetAttribute(tc_gemm_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM);
-        attr = true;
-    }
-    KTimer kt(KC_TCGEMM, s, 2.0 * M * N * K, 2.0 * ((double)M * K + (double)N * K + (beta != 0.f ? 2.0 : 1.0) * M * N));
-    static int nsm = 0;
-    if (nsm == 0) {
-        int dev;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(tc_gemm_persistent_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::PSMEM);
         cudaFuncSetAttribute(tc_gemm_persistent_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::PSMEM);
-    }
+        return v;
+    }();
+    KTimer kt(KC_TCGEMM, s, 2.0 * M * N * K, 2.0 * ((double)M * K + (double)N * K + (beta != 0.f ? 2.0 : 1.0) * M * N));
     const int tiles = (int)(grid.x * grid.y);
     if (ctma && tiles >= nsm && !env_flag("LYAP_TC_NONPERSISTENT")) {
         const int g = std::min(tiles, max_ctas > 0 ? std::min(max_ctas, nsm) : nsm);
