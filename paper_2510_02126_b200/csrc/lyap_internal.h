@@ -38,6 +38,9 @@ template <typename T> int gemm_update(cudaStream_t s, int n, int b, const T *X, 
 struct QrWork {
     int mmax = 0, nmax = 0;
     double *V = nullptr, *T = nullptr, *W = nullptr, *tau = nullptr, *Wk = nullptr;
+    double *gin = nullptr;     // global inbox of the grid-cooperative panel
+    double *Tbig = nullptr, *G = nullptr, *W1 = nullptr, *W2 = nullptr;   // two-level blocking
+    int gin_ctas = 0;
     int alloc(int mmax, int nmax);
     void release();
 };

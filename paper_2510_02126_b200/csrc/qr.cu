@@ -13,6 +13,7 @@
 // The sign convention diag(R) >= 0 makes the factorization unique for full
 // column rank, so it matches any other Householder QR up to rounding.
 #include <vector>
+#include <type_traits>
 #include <cooperative_groups.h>
 #include "common.cuh"
 #include "gemm_simt.cuh"
@@ -23,6 +24,7 @@
 namespace lyap {
 
 static constexpr int QB = 32;
+constexpr int QB2 = 256;      // outer block of the two-level blocking
 
 // Warp reduce-scatter: lane l ends with sum over the warp of d[l].  31 shuffles.
 __device__ __forceinline__ double reduce_scatter32(double (&d)[QB], int lane)
@@ -363,10 +365,40 @@ constexpr int QRT = 256, QNV = QB + 5;
 __device__ unsigned long long g_qr_fallbacks = 0, g_qr_reflectors = 0;
 #endif     // 32 dots + S_xx, S_vx, S_vv, x_{j+1}, v_{j+1}
 
-template <int NV>
-__device__ __forceinline__ void qr_cta_reduce_push(double (&vals)[NV], int lane, int wid, int q, int NC,
-                                                   double (*part)[NV + 1], double (*inbox)[NV + 1],
-                                                   cooperative_groups::cluster_group &cl)
+// Exchange of the per-CTA partial sums of one reflector step between the CTAs that
+// hold the panel rows.  Cluster flavour (R <= 16 x 256 rows): every CTA pushes its
+// partials into every CTA's shared-memory inbox (DSMEM) and one cluster barrier
+// publishes them.  Grid flavour (taller panels, a cooperative launch of ceil(R/256)
+// CTAs): every CTA stores its partials once in a global inbox and one grid barrier
+// publishes them.  Both inboxes are double-buffered by step parity (a fast CTA writes
+// step j+1's partials while a slow one may still read step j's); every CTA then sums
+// the NC partials of a slot in the same fixed order (deterministic).
+struct QrXCluster {
+    cooperative_groups::cluster_group cl;
+    double (*inbox)[16][QNV + 1];                  // shared [2][16][QNV + 1]
+    int q, NC;
+    __device__ QrXCluster(double (*ib)[16][QNV + 1], double *)
+        : cl(cooperative_groups::this_cluster()), inbox(ib), q((int)cl.block_rank()), NC((int)cl.num_blocks()) {}
+    __device__ void put(int buf, int slot, double v) {
+        for (int r = 0; r < NC; r++) cl.map_shared_rank(&inbox[buf][0][0], r)[q * (QNV + 1) + slot] = v;
+    }
+    __device__ double get(int buf, int r, int slot) const { return inbox[buf][r][slot]; }
+    __device__ void sync() { cl.sync(); }
+};
+struct QrXGrid {
+    cooperative_groups::grid_group g;
+    double *gin;                                   // global [2][NC][QNV + 1]
+    int q, NC;
+    __device__ QrXGrid(double (*)[16][QNV + 1], double *g_in)
+        : g(cooperative_groups::this_grid()), gin(g_in), q((int)blockIdx.x), NC((int)gridDim.x) {}
+    __device__ void put(int buf, int slot, double v) { gin[((long)buf * NC + q) * (QNV + 1) + slot] = v; }
+    __device__ double get(int buf, int r, int slot) const { return __ldcg(gin + ((long)buf * NC + r) * (QNV + 1) + slot); }
+    __device__ void sync() { g.sync(); }
+};
+
+template <int NV, class X>
+__device__ __forceinline__ void qr_cta_reduce_push(double (&vals)[NV], int lane, int wid, int buf,
+                                                   double (*part)[NV + 1], X &x)
 {
     // lanes: reduce-scatter of the first 32 values, plain sums of the rest (lane 0)
     double d[QB];
@@ -388,25 +420,37 @@ __device__ __forceinline__ void qr_cta_reduce_push(double (&vals)[NV], int lane,
     if (t < NV) {
         double acc = 0.0;
         for (int w = 0; w < QRT / 32; w++) acc += part[w][t];
-        for (int r = 0; r < NC; r++) cl.map_shared_rank(&inbox[0][0], r)[q * (NV + 1) + t] = acc;
+        x.put(buf, t, acc);
     }
-    cl.sync();
+    x.sync();
 }
 
+// Sum over the NC CTAs of inbox slot `slot` (fixed order r = 0..NC-1).
+template <class X>
+__device__ __forceinline__ double qr_gather(const X &x, int buf, int slot)
+{
+    double acc = 0.0;
+    for (int r = 0; r < x.NC; r++) acc += x.get(buf, r, slot);
+    return acc;
+}
+
+template <bool GRID>
 __global__ void __launch_bounds__(QRT)
 qr_panel_reg_kernel(int m, int j0, int jb, double *__restrict__ W, double *__restrict__ V,
-                    double *__restrict__ tau, double *__restrict__ diag, double *__restrict__ Tp)
+                    double *__restrict__ tau, double *__restrict__ diag, double *__restrict__ Tp,
+                    double *__restrict__ gin)
 {
     namespace cg = cooperative_groups;
-    cg::cluster_group cl = cg::this_cluster();
-    const int q = (int)cl.block_rank(), NC = (int)cl.num_blocks();
+    using X = std::conditional_t<GRID, QrXGrid, QrXCluster>;
+    __shared__ double inbox_sh[GRID ? 1 : 2][16][QNV + 1];
+    X x(inbox_sh, gin);
+    const int q = x.q;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int R = m - j0;
     const int gi = q * QRT + tid;                          // this thread's panel row
     const bool has = gi < R;
     __shared__ double part[QRT / 32][QNV + 1];
-    __shared__ double inbox[2][16][QNV + 1];
-    __shared__ double tot[QNV];
+    __shared__ double tot[QNV + 1];
     __shared__ double G[QB][QB + 1];
     __shared__ double tl[QB];
     double row[QB];
@@ -423,11 +467,12 @@ qr_panel_reg_kernel(int m, int j0, int jb, double *__restrict__ W, double *__res
         if (tid < 2) {
             double acc = 0.0;
             for (int w = 0; w < QRT / 32; w++) acc += part[w][tid];
-            for (int r = 0; r < NC; r++) cl.map_shared_rank(&inbox[1][0][0], r)[q * (QNV + 1) + tid] = acc;
+            x.put(1, tid, acc);
         }
-        cl.sync();
-        s = 0.0; x0 = 0.0;
-        for (int r = 0; r < NC; r++) { s += inbox[1][r][0]; x0 += inbox[1][r][1]; }
+        x.sync();
+        if (tid < 2) tot[tid] = qr_gather(x, 1, tid);
+        __syncthreads();
+        s = tot[0]; x0 = tot[1];
         __syncthreads();
     }
     for (int jj = 0; jj < jb; jj++) {
@@ -453,12 +498,8 @@ qr_panel_reg_kernel(int m, int j0, int jb, double *__restrict__ W, double *__res
         vals[QB + 2] = below ? vi * vi : 0.0;
         vals[QB + 3] = (has && gi == jj + 1) ? xn : 0.0;
         vals[QB + 4] = (has && gi == jj + 1) ? vi : 0.0;
-        qr_cta_reduce_push<QNV>(vals, lane, wid, q, NC, part, inbox[buf], cl);
-        if (tid < QNV) {
-            double acc = 0.0;
-            for (int r = 0; r < NC; r++) acc += inbox[buf][r][tid];
-            tot[tid] = acc;
-        }
+        qr_cta_reduce_push<QNV>(vals, lane, wid, buf, part, x);
+        if (tid < QNV) tot[tid] = qr_gather(x, buf, tid);
         __syncthreads();
         if (q == 0 && tid < jj) G[tid][jj] = tot[tid];
         if (tid == 0) {
@@ -496,11 +537,12 @@ qr_panel_reg_kernel(int m, int j0, int jb, double *__restrict__ W, double *__res
                 if (tid == 0) {
                     double acc = 0.0;
                     for (int w = 0; w < QRT / 32; w++) acc += part[w][0];
-                    for (int r = 0; r < NC; r++) cl.map_shared_rank(&inbox[buf ^ 1][0][0], r)[q * (QNV + 1) + QNV] = acc;
+                    x.put(buf ^ 1, QNV, acc);
                 }
-                cl.sync();
-                s = 0.0;
-                for (int r = 0; r < NC; r++) s += inbox[buf ^ 1][r][QNV];
+                x.sync();
+                if (tid == 0) tot[QNV] = qr_gather(x, buf ^ 1, QNV);
+                __syncthreads();
+                s = tot[QNV];
             }
         }
         __syncthreads();
@@ -538,7 +580,7 @@ qr_panel_reg_kernel(int m, int j0, int jb, double *__restrict__ W, double *__res
 #pragma unroll
         for (int c = 0; c < QB; c++) Tp[a + c * QB] = Ta[c];
     }
-    cl.sync();
+    if constexpr (!GRID) x.sync();                 // no CTA leaves while its shared memory may be read
 }
 
 __global__ void set_identity_kernel(int m, int k, double *Q) {
@@ -580,9 +622,20 @@ int QrWork::alloc(int mmax_, int nmax_) {
     LYAP_CUDA_TRY(cudaMalloc(&W, sizeof(double) * (size_t)2 * QB * (nmax > mmax ? nmax : mmax)));
     LYAP_CUDA_TRY(cudaMalloc(&tau, sizeof(double) * (size_t)2 * kmax));
     LYAP_CUDA_TRY(cudaMalloc(&Wk, sizeof(double) * (size_t)mmax * nmax));
+    gin_ctas = ceil_div(mmax, QRT);
+    LYAP_CUDA_TRY(cudaMalloc(&gin, sizeof(double) * (size_t)2 * gin_ctas * (QNV + 1)));
+    if (kmax > QB2) {
+        LYAP_CUDA_TRY(cudaMalloc(&Tbig, sizeof(double) * (size_t)QB2 * QB2 * (kmax / QB2 + 1)));
+        LYAP_CUDA_TRY(cudaMalloc(&G, sizeof(double) * (size_t)QB2 * QB2));
+        LYAP_CUDA_TRY(cudaMalloc(&W1, sizeof(double) * (size_t)QB2 * nmax));
+        LYAP_CUDA_TRY(cudaMalloc(&W2, sizeof(double) * (size_t)QB2 * nmax));
+    }
     return LYAP_OK;
 }
-void QrWork::release() { cudaFree(V); cudaFree(T); cudaFree(W); cudaFree(tau); cudaFree(Wk); V = T = W = tau = Wk = nullptr; }
+void QrWork::release() {
+    for (double *p : {V, T, W, tau, Wk, gin, Tbig, G, W1, W2}) if (p) cudaFree(p);
+    V = T = W = tau = Wk = gin = Tbig = G = W1 = W2 = nullptr;
+}
 
 // alpha_j from the reflector: v = x - alpha e1 and tau = 2/(v^T v), ||v||^2 = 2 ||x||(||x|| + |x0|)
 // -> with v0 = x0 - alpha, alpha = -sign(x0) ||x||:  v0 = x0 + sign(x0)||x||, so
@@ -602,6 +655,63 @@ __global__ void qr_alpha_kernel(int m, int j0, int jb, const double *__restrict_
     }
 }
 
+// Compact-WY factor of an outer block of up to QB2 = 256 reflectors (8 panels of 32):
+// T = [[T_11, T_12], [0, T_22]] with the panel factors T_bb (from the panel kernels) on
+// the diagonal and, block column by block column,
+//     T(0:32b, b) = -T(0:32b, 0:32b) (G(0:32b, b) T_bb),   G = V^T V,
+// the LAPACK xLARFT recurrence taken 32 columns at a time.  One CTA; T (ld QB2) is
+// upper triangular with zeros below the diagonal.
+__global__ void __launch_bounds__(1024)
+qr_bigT_kernel(int Jb, const double *__restrict__ G, const double *__restrict__ Tsmall, double *__restrict__ Tb)
+{
+    extern __shared__ double m1_sm[];
+    double (*M1)[QB + 1] = reinterpret_cast<double (*)[QB + 1]>(m1_sm);   // [QB2 - QB][QB + 1]
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int nb = (Jb + QB - 1) / QB;
+    for (int e = tid; e < QB2 * QB2; e += nt) {
+        const int i = e % QB2, c = e / QB2;
+        const int bi = i / QB, bc = c / QB;
+        Tb[e] = (bi == bc && i < Jb && c < Jb) ? Tsmall[(long)bc * QB * QB + (i % QB) + (c % QB) * QB] : 0.0;
+    }
+    __syncthreads();
+    for (int b = 1; b < nb; b++) {
+        const int r = QB * b, cb = min(QB, Jb - r);
+        const double *Tbb = Tsmall + (long)b * QB * QB;
+        for (int e = tid; e < r * QB; e += nt) {
+            const int i = e % r, c = e / r;
+            double acc = 0.0;
+            if (c < cb)
+                for (int l = 0; l <= c; l++) acc = fma(G[i + (long)(r + l) * Jb], Tbb[l + c * QB], acc);
+            M1[i][c] = acc;
+        }
+        __syncthreads();
+        for (int e = tid; e < r * QB; e += nt) {
+            const int i = e % r, c = e / r;
+            if (c < cb) {
+                double acc = 0.0;
+                for (int l = i; l < r; l++) acc = fma(Tb[i + (long)l * QB2], M1[l][c], acc);
+                Tb[i + (long)(r + c) * QB2] = -acc;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// C (rows row0..m-1, ncols columns, ld ldc) <- (I - V op(T) V^T) C with the outer-block
+// reflectors V (rows row0.., Jb columns, ld ldv) and T (ld QB2): three DMMA GEMMs,
+// op(T) = T^T for Q^T (trans = 1) and T for Q (trans = 0).
+static int qr_block_apply(cudaStream_t s, int m, int row0, int ncols, int Jb, const double *V, int ldv,
+                          const double *Tb, int trans, double *C, int ldc, double *W1, double *W2)
+{
+    if (ncols <= 0) return LYAP_OK;
+    const int mr = m - row0;
+    const double *Vs = V + row0;
+    double *Cs = C + row0;
+    LYAP_TRY(dgemm_cm(s, true, false, Jb, ncols, mr, 1.0, Vs, ldv, Cs, ldc, 0.0, W1, Jb));
+    LYAP_TRY(dgemm_cm(s, trans != 0, false, Jb, ncols, Jb, 1.0, Tb, QB2, W1, Jb, 0.0, W2, Jb));
+    return dgemm_cm(s, false, false, mr, ncols, Jb, -1.0, Vs, ldv, W2, Jb, 1.0, Cs, ldc);
+}
+
 int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, QrWork &w)
 {
     if (m <= 0 || n <= 0) return LYAP_OK;
@@ -618,29 +728,39 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
     }();
     (void)attr;
     LYAP_CUDA_TRY(cudaMemcpyAsync(Wm, A, sizeof(double) * (size_t)m * n, cudaMemcpyDeviceToDevice, s));
-    // cluster panels (32 wide) while a CTA's row slice fits in shared memory; otherwise
-    // the one-CTA panel with widths 32, or 16/8 while the panel would not fit
+    // register panels (32 wide, one row per thread): a cluster of up to 16 CTAs for R <=
+    // 4096 panel rows, a cooperative grid of ceil(R / 256) co-resident CTAs above; the
+    // shared-memory cluster panel and the one-CTA panel (widths 32, or 16/8 while the panel
+    // would not fit) remain for panels taller than one co-resident grid
+    static const int grid_max = [] {
+        int dev = 0, nsm = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(qr_panel_reg_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, qr_panel_reg_kernel<true>, QRT, 0);
+        return nsm * std::max(per, 0);
+    }();
+    const bool use_grid = ceil_div(m, QRT) <= std::min(grid_max, w.gin_ctas) && !env_flag("LYAP_QR_NOGRID");
     const bool use_cluster = ceil_div(m, QC) * QB * sizeof(double) <= 200 * 1024 && !env_flag("LYAP_QR_1CTA");
     std::vector<int> starts;
     for (int j0 = 0, jb; j0 < k; j0 += jb) {
         jb = QB;
-        while (!use_cluster && jb > 8 && sizeof(double) * (size_t)(m - j0) * jb > 200 * 1024) jb /= 2;
+        while (!use_cluster && !use_grid && jb > 8 && sizeof(double) * (size_t)(m - j0) * jb > 200 * 1024) jb /= 2;
         jb = std::min(jb, k - j0);
         starts.push_back(j0);
     }
     starts.push_back(k);
+    // two-level blocking for tall, wide factorizations (all panels 32 wide), one level
+    // below (measured: the per-panel fused application wins while the matrix sits in L2)
+    bool two_level = (use_grid || use_cluster) && (long)m * n >= (1L << 22) && k > QB2 && w.Tbig != nullptr;
+    if (env_flag("LYAP_QR_1LEVEL")) two_level = false;
+    if (env_flag("LYAP_QR_2LEVEL") && (use_grid || use_cluster) && w.Tbig) two_level = true;
     for (size_t pi = 0; pi + 1 < starts.size(); pi++) {
         const int j0 = starts[pi], jb = starts[pi + 1] - j0;
         double *Tp = w.T + pi * QB * QB;
         if (m - j0 <= 16 * QRT && !env_flag("LYAP_QR_SMEM")) {
             const int nc = ceil_div(m - j0, QRT);
             KTimer kp(KC_QR_PANEL, s, 4.0 * (m - j0) * jb * jb, 16.0 * (m - j0) * jb);
-            // one-time setup (function-local static: thread-safe initialisation)
-            static const bool attr_r = [] {
-                cudaFuncSetAttribute(qr_panel_reg_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-                return true;
-            }();
-            (void)attr_r;
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(nc, 1, 1);
             cfg.blockDim = dim3(QRT, 1, 1);
@@ -652,7 +772,16 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
             at[0].val.clusterDim.z = 1;
             cfg.attrs = at;
             cfg.numAttrs = 1;
-            LYAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel, m, j0, jb, Wm, w.V, w.tau, diag, Tp));
+            LYAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, qr_panel_reg_kernel<false>, m, j0, jb, Wm, w.V, w.tau, diag, Tp,
+                                             (double *)nullptr));
+            LYAP_TRY(launched());
+        } else if (use_grid) {
+            const int nc = ceil_div(m - j0, QRT);
+            KTimer kp(KC_QR_PANEL, s, 4.0 * (m - j0) * jb * jb, 16.0 * (m - j0) * jb);
+            int mm = m, jj0 = j0, jjb = jb;
+            double *Wp = Wm, *Vp = w.V, *tp = w.tau, *dp = diag, *Tq = Tp, *gp = w.gin;
+            void *args[] = {&mm, &jj0, &jjb, &Wp, &Vp, &tp, &dp, &Tq, &gp};
+            LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)qr_panel_reg_kernel<true>, dim3(nc), dim3(QRT), args, 0, s));
             LYAP_TRY(launched());
         } else if (use_cluster) {
             const int RB = ceil_div(m - j0, QC);
@@ -672,24 +801,53 @@ int qr_f64(cudaStream_t s, int m, int n, const double *A, double *Q, double *R, 
             qr_alpha_kernel<<<1, 32, 0, s>>>(m, j0, jb, w.V, w.tau, diag);
             LYAP_TRY(launched());
         }
-        int nt = n - (j0 + jb);
+        // two-level: the panel's reflectors update the rest of their outer block (wy_apply);
+        // at the end of an outer block its 256 reflectors update the trailing columns at
+        // once (G = V^T V, T_big, three DMMA GEMMs).  One level: every panel updates all
+        // trailing columns.
+        const int J0 = two_level ? (j0 / QB2) * QB2 : j0;
+        const int Jend = two_level ? std::min(J0 + QB2, k) : n;
+        int nt = std::min(n, Jend) - (j0 + jb);
         if (nt > 0) {
             const double *Vp = w.V + (size_t)j0 * m;
             double *Wt = Wm + (size_t)(j0 + jb) * m;
             // Wt <- (I - V T^T V^T) Wt, rows j0..m-1 (V is zero above)
             LYAP_TRY(wy_apply(s, m, nt, jb, j0, Vp, m, Tp, 1, Wt, m));
         }
+        if (two_level && j0 + jb == Jend) {
+            const int Jb = Jend - J0, ob = J0 / QB2;
+            const double *Vb = w.V + (size_t)J0 * m;
+            double *Tb = w.Tbig + (size_t)ob * QB2 * QB2;
+            LYAP_TRY(dgemm_cm(s, true, false, Jb, Jb, m - J0, 1.0, Vb + J0, m, Vb + J0, m, 0.0, w.G, Jb));
+            constexpr size_t bigT_smem = sizeof(double) * (QB2 - QB) * (QB + 1);
+            static const bool bigT_attr = [] {
+                cudaFuncSetAttribute(qr_bigT_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bigT_smem);
+                return true;
+            }();
+            (void)bigT_attr;
+            qr_bigT_kernel<<<1, 1024, bigT_smem, s>>>(Jb, w.G, w.T + (size_t)(J0 / QB) * QB * QB, Tb);
+            LYAP_TRY(launched());
+            LYAP_TRY(qr_block_apply(s, m, J0, n - Jend, Jb, Vb, m, Tb, 1, Wm + (size_t)Jend * m, m, w.W1, w.W2));
+        }
     }
     // Q = H_0 ... H_{k-1} [I; 0]
     set_identity_kernel<<<ceil_div((long)m * k, 256) < 1024 ? ceil_div((long)m * k, 256) : 1024, 256, 0, s>>>(m, k, Q);
     LYAP_TRY(launched());
-    for (int pi = (int)starts.size() - 2; pi >= 0; pi--) {
-        const int j0 = starts[pi], jb = starts[pi + 1] - j0;
-        const double *Tp = w.T + (size_t)pi * QB * QB;
-        const double *Vp = w.V + (size_t)j0 * m;
-        int nc = k - j0;               // columns j0..k-1 of Q are affected
-        double *Qc = Q + (size_t)j0 * m;
-        LYAP_TRY(wy_apply(s, m, nc, jb, j0, Vp, m, Tp, 0, Qc, m));
+    if (two_level) {
+        for (int ob = (k - 1) / QB2; ob >= 0; ob--) {
+            const int J0 = ob * QB2, Jb = std::min(QB2, k - J0);
+            LYAP_TRY(qr_block_apply(s, m, J0, k - J0, Jb, w.V + (size_t)J0 * m, m, w.Tbig + (size_t)ob * QB2 * QB2, 0,
+                                    Q + (size_t)J0 * m, m, w.W1, w.W2));
+        }
+    } else {
+        for (int pi = (int)starts.size() - 2; pi >= 0; pi--) {
+            const int j0 = starts[pi], jb = starts[pi + 1] - j0;
+            const double *Tp = w.T + (size_t)pi * QB * QB;
+            const double *Vp = w.V + (size_t)j0 * m;
+            int nc = k - j0;               // columns j0..k-1 of Q are affected
+            double *Qc = Q + (size_t)j0 * m;
+            LYAP_TRY(wy_apply(s, m, nc, jb, j0, Vp, m, Tp, 0, Qc, m));
+        }
     }
     int tot = (int)(((long)k * n + (long)m * k + 255) / 256);
     qr_finish_kernel<<<tot < 1024 ? tot : 1024, 256, 0, s>>>(m, n, k, Wm, diag, Q, R);
