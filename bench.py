@@ -123,61 +123,82 @@ def dist_env():
 
 
 # ------------------------------------------------------------------ reference arm (oracle)
+REF_N = {"cfg0": 64, "cfg1": 192, "cfg2": 100, "cfg4": 192}
+
+
+def _oracle_solve(p, us, imax):
+    import oracle
+    with oracle.model("tc"):
+        if p.S is not None:
+            return oracle.ir_ldlt(p.A, p.L, p.S, us=us, tol=1e-14, imax=imax)
+        return oracle.ir_chol(p.A, p.L, us=us, tol=1e-14, imax=imax)
+
+
+def _reduced_problem(config, n):
+    import problems as P
+    if config == "cfg2":
+        return P.cfg2(g=int(round(n ** 0.5)))
+    if config == "cfg4":
+        return P.cfg4_member(0, n=n)
+    return getattr(P, config)(n=n)
+
+
 def run_reference(args):
+    """Reference arm = the CPU oracle (oracle/, plain C, tc precision model) as it stands,
+    one host core.  Each step is one COMPLETE IR solve (A-sequence, Z-sides, residual
+    factorizations, solution updates) of the same recipe at a reduced order n (the
+    oracle needs ~20 min for n = 1024); value = solves/s of exactly that timed work."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    import numpy as np
     import oracle
-    import problems as P
-    if args.config == "cfg4":
-        wl = dict(us="fp16", desc="configs[4] member 0 (n=2048 m=4 Cholesky fp16, kappa 10)")
-        p = P.cfg4_member(0)
-    else:
-        wl = WORKLOADS[args.config]
-        p = getattr(P, wl["gen"])()
-    A = p.A
+    cfgname = args.config if args.config in REF_N else "cfg1"
+    n = REF_N[cfgname]
+    p = _reduced_problem(cfgname, n)
+    us = {"cfg0": "fp16", "cfg1": "bf16", "cfg2": "fp16", "cfg4": "fp16"}[cfgname]
     oracle.lib()
-    # warm-up: the full A-side sequence gives the number of inversions per solve
-    t0 = time.perf_counter()
-    q = oracle.aseq(wl["us"], A)
-    k_inv = q.steps
-    t_aseq = time.perf_counter() - t0
-    for _ in range(max(0, args.warmup - 1)):
-        oracle.inverse(wl["us"], oracle.round_(A, wl["us"]))
-    times = []
-    Ar = oracle.round_(A, wl["us"])
+    for _ in range(max(0, args.warmup)):
+        _oracle_solve(p, us, 30)
+        break                                   # one warm-up solve (page-in); the rest are identical
+    times, r = [], None
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.inverse(wl["us"], Ar)
+        r = _oracle_solve(p, us, 30)
         times.append(time.perf_counter() - t0)
-    t_inv = sum(times) / len(times)
-    t_solve = t_inv * k_inv
+    t_solve = sum(times) / len(times)
     value = 1.0 / t_solve
-    sample = (f"one oracle inversion of A_0 per step (emulated {wl['us']}, chop model, n={p.n}); "
-              f"solve time = t_inv x {k_inv} inversions (the A-sequence length; the full A-sequence "
-              f"took {t_aseq:.1f} s); excludes Z-side and refinement work, so CPU throughput is overestimated")
+    desc = WORKLOADS[cfgname]["desc"] if cfgname in WORKLOADS else "configs[4] member"
+    sample = (f"one complete oracle IR solve per step (tc model, {us} solver, fp64 refinement) of the "
+              f"{cfgname} recipe at n={n} (status {r.status}, {r.steps} IR steps, {r.newton_total} Newton "
+              f"steps); 1 core; not extrapolated")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_solve,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": wl["us"],
-            "data": "synthetic", "config": {"workload": wl["desc"], "n": p.n, "m": p.m},
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": us,
+            "data": "synthetic", "config": {"workload": f"{desc} -- recipe at reduced n={n}", "n": n, "m": p.m},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def cpu_baseline_sample(wl, p, budget_s=30.0):
-    """Oracle as it stands on a bounded sample: the emulated A-side Newton sequence of the same
-    equation (k inversions), single-threaded C."""
-    import oracle
+def cpu_baseline_sample(config, budget_s=30.0):
+    """The oracle as it stands (tc model, one core) on a bounded sample: one complete IR
+    solve of the benched recipe at n = 256 (~20 s); value scaled to the benched n by the
+    method's n^3 cost (every phase is O(n^3) or O(n p^2) at ranks p ~ n / 10)."""
+    import problems as P
+    n_s = 256
+    p = P.cfg1(n=n_s) if config == "cfg1" else _reduced_problem(config, n_s)
+    us = WORKLOADS[config]["us"]
     t0 = time.perf_counter()
-    q = oracle.aseq(wl["us"], p.A)
+    r = _oracle_solve(p, us, 30)
     t = time.perf_counter() - t0
-    return {"value": 1.0 / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle sign-Newton A-sequence ({q.steps} emulated {wl['us']} inversions, chop model) "
-                      f"of the same n={p.n} equation, {t:.1f} s on 1 core; value = 1/that time (excludes the "
-                      f"Z-side and refinement work, i.e. an upper bound on oracle solves/s)"}
+    n_full = {"cfg0": 64, "cfg1": 1024, "cfg2": 4096}.get(config, 1024)
+    scale = (n_full / n_s) ** 3
+    return {"value": 1.0 / (t * scale), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"one complete oracle IR solve (tc model, {us}) of the {config} recipe at n={n_s}: "
+                      f"{t:.1f} s on 1 core ({r.status}, {r.steps} IR steps); value = 1 / (that time x "
+                      f"(n/{n_s})^3 = {scale:.0f})",
+            "measured_s_at_sample": t}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -382,12 +403,56 @@ def run_gpu(args):
     if args.scale in ("cfg2", "both"):
         line["sign_newton_at_scale" if args.scale == "cfg2" else "sign_newton_at_scale_cfg2"] = \
             sign_newton_scale(G, P, dev, pk, "cfg2")
+    if args.cfg3 != "none" and world == 1:
+        line["time_to_solution_cfg3"] = cfg3_solves(G, P, dev, args.cfg3)
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample(wl, p)
+        line["cpu_baseline"] = cpu_baseline_sample(args.config)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+CFG3_SOLVERS = {
+    "fp16": dict(max_cols=4096, newton_cols=8192, work_cols=10240),
+    "fp32": dict(max_cols=6144, newton_cols=14336, work_cols=16384),
+}
+
+
+def cfg3_solves(G, P, dev, which):
+    """configs[3] (n = 16384, m = 16, convection-diffusion 128 x 128, conv. 50) end to end
+    with the fp16 and the fp32 solver: one warm-up solve (workspace, inverse cache), then one
+    solve timed with CUDA events on the solver's stream; status, IR steps, residuals, ranks
+    and the phase split are the library's report."""
+    import numpy as np
+    import torch
+    p = P.cfg3()
+    A = torch.tensor(p.A, dtype=torch.float64, device=dev)
+    Lt = torch.tensor(np.ascontiguousarray(p.L.T), dtype=torch.float64, device=dev)
+    out = {"workload": "configs[3]: n=16384 m=16 Cholesky, convection-diffusion 128x128 (conv 50), "
+                       "L ~ N(0,1), tol 1e-14, maxit 10"}
+    for us in (["fp16", "fp32"] if which == "both" else [which]):
+        s = G.Solver(p.n, us=us, **CFG3_SOLVERS[us])
+        s.solve(A, Lt, None, tol=1e-14, maxit=10)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = s.solve(A, Lt, None, tol=1e-14, maxit=10)
+        e1.record()
+        torch.cuda.synchronize()
+        rep = r.report
+        ms = e0.elapsed_time(e1)
+        out[us] = {"ms": ms, "status": rep["status"], "ir_steps": rep["steps"], "inversions": rep["inversions"],
+                   "newton_steps_per_call": rep["newton_steps"], "res": rep["res"], "ranks": rep["ranks"],
+                   "final_rel_residual": rep["final_res"], "rank": rep["rank"],
+                   "phase_ms": {"newton": rep["newton_ms"], "residual": rep["residual_ms"],
+                                "update": rep["update_ms"]},
+                   "sign_newton_tflops": rep["newton_flops"] / (rep["newton_ms"] / 1e3) / 1e12}
+        del s, r
+        torch.cuda.empty_cache()
+    del A, Lt
+    torch.cuda.empty_cache()
+    return out
 
 
 def sign_newton_scale(G, P, dev, pk, which):
@@ -461,12 +526,16 @@ def run_batch(args):
     importlib_build()
     import paper_2510_02126_b200 as G
     import problems as P
-    E = args.eq_per_gpu
-    per_group = max(1, E // 4)
-    pool = B.stratified(256, 4, 64)                         # all 256, group-major
-    # weak scaling: rank r takes members r*per_group .. of every kappa group
-    idx = [g * 64 + (rank * per_group + i) % 64 for g in range(4) for i in range(per_group)][:E]
-    del pool
+    # configs[4] at spec: the 256 equations (four kappa groups of 64) sharded evenly over the
+    # ranks (256 / N each); --eq-per-gpu E < 256/N runs a stratified E-member sample instead
+    full = B.shard(256, rank, world)
+    E = args.eq_per_gpu if args.eq_per_gpu > 0 else len(full)
+    if E >= len(full):
+        idx = full
+    else:
+        per_group = max(1, E // 4)
+        idx = [g * 64 + (rank * per_group + i) % 64 for g in range(4) for i in range(per_group)][:E]
+    E = len(idx)
     probs = [P.cfg4_member(i) for i in idx]
     n = probs[0].n
     lanes = max(1, min(args.lanes, E))
@@ -487,10 +556,13 @@ def run_batch(args):
                 "ok": 1.0 if rep["status"] == "converged" else 0.0}
 
     items = list(range(E))
-    for k in items:                               # first warm-up pass sequential (one-time setup)
-        work(k, k % lanes)
-    for _ in range(args.warmup - 1):
-        B.run_concurrent(work, items, lanes)
+    # warm-up: every handle solves once (one-time setup, sequential), then W concurrent passes
+    # over a stratified sample of at most 8 of this rank's equations (a full pass is ~1 min)
+    warm = sorted(set(items[:: max(1, E // 8)]))[:8]
+    for ln in range(lanes):
+        work(warm[ln % len(warm)], ln)
+    for _ in range(args.warmup):
+        B.run_concurrent(work, warm, lanes)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -534,7 +606,9 @@ def run_batch(args):
         "warmup": args.warmup, "ms_per_step": tmax / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp16", "data": "synthetic",
         "config": {"workload": f"configs[4] batch: n=2048 m=4 Cholesky fp16, {E} equations per GPU per step "
-                               f"(kappa groups 1e1..1e4), {lanes} concurrent solver handles/streams per GPU",
+                               f"({world * E} of 256 per step, kappa groups 1e1..1e4), {lanes} concurrent "
+                               f"solver handles/streams per GPU; warm-up = {args.warmup} passes over "
+                               f"{len(warm)} of them",
                    "n": n, "equations_per_gpu": E, "lanes": lanes, "parallelism": f"dp{world}",
                    "l2": "inputs (32 MB A per equation) exceed L2 together; no flush"},
         "equations": allres, "all_converged": all(r["ok"] == 1.0 for r in allres),
@@ -561,9 +635,12 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg1", choices=sorted(WORKLOADS) + ["cfg4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--eq-per-gpu", type=int, default=4, help="configs[4]: equations per GPU per step")
-    ap.add_argument("--lanes", type=int, default=4, help="configs[4]: concurrent solver handles per GPU")
+    ap.add_argument("--eq-per-gpu", type=int, default=0,
+                    help="configs[4]: equations per GPU per step (0 = 256 / N, the full batch)")
+    ap.add_argument("--lanes", type=int, default=6, help="configs[4]: concurrent solver handles per GPU")
     ap.add_argument("--max-cols", type=int, default=1536, help="configs[4]: factor capacity per handle")
+    ap.add_argument("--cfg3", default="both", choices=["none", "fp16", "fp32", "both"],
+                    help="also solve configs[3] end to end with these solver precisions (rank 0 of N=1)")
     ap.add_argument("--scale", default="both", choices=["none", "cfg2", "cfg3", "both"],
                     help="also time the fp16 sign-Newton A-sequence at this configuration's n (rank 0)")
     args = ap.parse_args()

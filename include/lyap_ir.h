@@ -54,7 +54,9 @@ extern "C" {
 /* Algorithmic parameters (Section 4.1 l.1419-1428 for defaults). */
 typedef struct {
     int    kmax;        /* max Newton steps per solve (l.1422: 50) */
-    int    scaling;     /* Frobenius-norm scaling (l.1139, l.1406): 1 */
+    int    scaling;     /* mu_k (l.1139): 0 none, 1 Frobenius-norm scaling (the
+                           paper's choice, l.1406; default), 2 determinantal
+                           scaling |det A_k|^{-1/n} from the inversion's pivots */
     int    extra;       /* Newton iterations after Eq. newton-stop-tau holds
                            (reading R-EXTRA: 1, matches Table 4) */
     double rho;         /* rank truncation threshold rho (l.1424: 0.1) */
@@ -62,6 +64,10 @@ typedef struct {
     double eta_s;       /* solution truncation, relative (l.1427: 10u) */
     int    cache;       /* reuse the A_k^{-1} sequence across refinement steps
                            (Section 3.4, l.1358-1375): 1 */
+    int    newton_cols; /* capacity of the Newton factor Z_k (columns before a
+                           truncation); 0 = 2 max(2 max_cols + 64, ceil(rho n)) + 16 */
+    int    work_cols;   /* capacity of the fp64 residual / update factors
+                           ([Z, AZ, L] and [Z, Z_+, Z_-]); 0 = newton_cols + 2 max_cols + 64 */
 } lyap_ir_options;
 
 /* Per-solve report. */
@@ -101,6 +107,10 @@ int lyap_ir_destroy(lyap_ir_handle h);
  *   A  device, row-major n x n fp64          (read only)
  *   L  device, column-major n x m fp64       (read only)
  *   S  device, column-major m x m fp64 or NULL
+ *   us solver precision u_s (LYAP_FP64/FP32/FP16/BF16, Table 3 l.1078), or -1 for
+ *      the handle's current one; a different u_s re-allocates the u_s-typed
+ *      workspace and drops the cached A_k^{-1} sequence
+ *   ur residual precision u_r: LYAP_FP64 (the only supported value)
  *   tol  relative-residual tolerance (Eq. res-fac-sol), maxit = i_max
  *   Z  device, column-major n x max_cols fp64 (output, first *rank columns)
  *   Y  device, column-major max_cols x max_cols fp64 (output; LDL^T only,
@@ -111,13 +121,13 @@ int lyap_ir_destroy(lyap_ir_handle h);
  * outgrowing max_cols later in rep->status = LYAP_STATUS_CAPACITY, both with the last
  * iterate returned. */
 int lyap_ir_solve(lyap_ir_handle h, const double *A, const double *L, int m,
-                  const double *S, int ur, double tol, int maxit,
+                  const double *S, int us, int ur, double tol, int maxit,
                   double *Z, double *Y, int *rank, lyap_ir_report *rep);
 
 /* Same, with HOST buffers: copies A, L, S host->device and Z, Y back inside
  * the call (the end-to-end path). */
 int lyap_ir_solve_host(lyap_ir_handle h, const double *A, const double *L, int m,
-                       const double *S, int ur, double tol, int maxit,
+                       const double *S, int us, int ur, double tol, int maxit,
                        double *Z, double *Y, int *rank, lyap_ir_report *rep);
 
 /* ---------------- individual steps of the hot path (for parity tests) ------ */

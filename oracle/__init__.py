@@ -83,6 +83,8 @@ def _declare(L):
     L.orc_getrf.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _ip]
     L.orc_inverse.restype = C.c_int
     L.orc_inverse.argtypes = [C.c_int, C.c_int, _dp, _dp, _ip]
+    L.orc_inverse_ld.restype = C.c_int
+    L.orc_inverse_ld.argtypes = [C.c_int, C.c_int, _dp, _dp, _ip, C.POINTER(C.c_double)]
     L.orc_qr.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]
     L.orc_syev.restype = C.c_int
     L.orc_syev.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp]
@@ -236,6 +238,17 @@ def inverse(p, A):
     return X, piv, info
 
 
+def inverse_logdet(p, A):
+    """(A^{-1}, pivots, info, log|det A|) from one LU with partial pivoting."""
+    A = _f(A)
+    n = A.shape[0]
+    X = np.zeros((n, n), order="F")
+    piv = np.zeros(n, dtype=np.int32)
+    ld = C.c_double(0.0)
+    info = lib().orc_inverse_ld(_prec(p), n, _p(A), _p(X), piv.ctypes.data_as(_ip), C.byref(ld))
+    return X, piv, info, ld.value
+
+
 def qr(p, A):
     A = _f(A)
     m, n = A.shape
@@ -288,8 +301,14 @@ class ASeq:
     handle: int = field(repr=False, default=0)
 
 
+SCALINGS = {"none": 0, "fro": 1, "det": 2}
+
+
 def newton_params(kmax=50, scaling=True, extra=1, rho=0.1) -> NewtonParams:
-    return NewtonParams(kmax, int(scaling), extra, rho)
+    """scaling: False/"none" (mu = 1), True/"fro" (Frobenius norm, l.1406), "det"
+    (|det A_k|^{-1/n}, l.1139)."""
+    sc = SCALINGS[scaling] if isinstance(scaling, str) else int(scaling)
+    return NewtonParams(kmax, sc, extra, rho)
 
 
 def aseq(p, A, kmax=50, scaling=True, extra=1, keep=False):

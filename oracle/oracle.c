@@ -184,13 +184,20 @@ int orc_getrf(int p, int n, double *A, int lda, int *piv)
     return 0;
 }
 
-int orc_inverse(int pout, int n, const double *A, double *Ainv, int *piv_out)
+/* Inverse and, if logabsdet != NULL, log|det A| = sum_i log|u_ii| from the same LU
+ * (for the determinantal scaling mu_k = |det A_k|^{-1/n}, l.1139). */
+int orc_inverse_ld(int pout, int n, const double *A, double *Ainv, int *piv_out, double *logabsdet)
 {
     const int p = acc_prec(pout);   /* TC model: eliminations in fp32, result stored in u_s */
     double *LU = dcopy(A, (long)n * n);
     int *piv = (int *)malloc(sizeof(int) * (n > 0 ? n : 1));
     int info = orc_getrf(p, n, LU, n, piv);
     if (info != 0) { free(LU); free(piv); return info; }
+    if (logabsdet) {
+        double ld = 0.0;
+        for (int i = 0; i < n; i++) ld += log(fabs(LU[IDX(i, i, n)]));
+        *logabsdet = ld;
+    }
     /* Solve A X = I column by column: X(:,j) = U^{-1} L^{-1} P e_j. */
     double *y = dalloc(n);
     for (int j = 0; j < n; j++) {
@@ -215,6 +222,11 @@ int orc_inverse(int pout, int n, const double *A, double *Ainv, int *piv_out)
     free(y); free(LU); free(piv);
     for (long t = 0; t < (long)n * n; t++) if (!isfinite(Ainv[t])) return -1;
     return 0;
+}
+
+int orc_inverse(int pout, int n, const double *A, double *Ainv, int *piv_out)
+{
+    return orc_inverse_ld(pout, n, A, Ainv, piv_out, NULL);
 }
 
 /* ------------------------------------------------------------------ */
@@ -511,12 +523,18 @@ orc_aseq *orc_aseq_compute(int p, int n, const double *A, const orc_newton_param
          * inverse of 2^-e A_k is 2^e A_k^{-1}; exact unless under/overflow */
         int e = exponent_of_max(nn, Ak);
         for (long t = 0; t < nn; t++) As[t] = ldexp(Ak[t], -e);
-        int r = orc_inverse(p, n, As, Ai, q->piv + (long)(it - 1) * n);
+        double ldw = 0.0;
+        int r = orc_inverse_ld(p, n, As, Ai, q->piv + (long)(it - 1) * n, &ldw);
         if (r != 0) { *info = r; break; }
         for (long t = 0; t < nn; t++) Ai[t] = FL(ldexp(Ai[t], -e));
         double mu = 1.0;
         int region_step = in_region;   /* convergence region reached at an earlier step */
-        if (scaling_on) {
+        if (scaling_on && P->scaling == 2) {
+            /* determinantal scaling mu = |det A_k|^{-1/n} (l.1139); det(2^-e A_k) = 2^{-en} det A_k */
+            double ld = ldw + (double)n * e * log(2.0);
+            if (isfinite(ld)) mu = exp(-ld / (double)n);
+            if (!(mu > 0.0) || !isfinite(mu)) mu = 1.0;
+        } else if (scaling_on) {
             double na = nrm_fro(nn, Ak), ni = nrm_fro(nn, Ai);
             if (na > 0.0 && ni > 0.0 && isfinite(na) && isfinite(ni)) mu = sqrt(ni / na);
         }

@@ -50,6 +50,8 @@ int orc_getrf(int prec, int n, double *A, int lda, int *piv);
 /* Ainv = A^{-1} via LU + solve against the identity, all at prec.
  * piv (may be NULL) receives the pivot sequence. Same return codes. */
 int orc_inverse(int prec, int n, const double *A, double *Ainv, int *piv);
+/* same, with log|det A| = sum log|u_ii| of the LU (NULL: not wanted) */
+int orc_inverse_ld(int prec, int n, const double *A, double *Ainv, int *piv, double *logabsdet);
 
 /* Thin Householder QR, k = min(m,n): Q (m x k), R (k x n) upper
  * trapezoidal with non-negative diagonal. */
@@ -72,7 +74,7 @@ int orc_rank_trunc_ldlt(int prec, int n, int c, const double *Z, const double *Y
 /* ---- sign-function Newton iteration (Section 3) ---- */
 typedef struct {
     int kmax;          /* maximal Newton steps (50) */
-    int scaling;       /* Frobenius-norm scaling on/off (l.1406) */
+    int scaling;       /* mu_k (l.1139): 0 none, 1 Frobenius norm (l.1406), 2 |det A_k|^{-1/n} */
     int extra;         /* iterations after tolerance (l.1312: 2) */
     double rho;        /* rank truncation threshold (l.1424: 0.1) */
 } orc_newton_params;

@@ -35,7 +35,8 @@ class LyapError(RuntimeError):
 
 class Options(C.Structure):
     _fields_ = [("kmax", C.c_int), ("scaling", C.c_int), ("extra", C.c_int), ("rho", C.c_double),
-                ("eta_r", C.c_double), ("eta_s", C.c_double), ("cache", C.c_int)]
+                ("eta_r", C.c_double), ("eta_s", C.c_double), ("cache", C.c_int),
+                ("newton_cols", C.c_int), ("work_cols", C.c_int)]
 
 
 MAXREP = 128
@@ -86,7 +87,7 @@ def lib():
         L.lyap_ir_default_options.restype = None
         L.lyap_ir_create.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.c_int, C.POINTER(Options), vp]
         L.lyap_ir_destroy.argtypes = [vp]
-        L.lyap_ir_solve.argtypes = [vp, dp, dp, C.c_int, dp, C.c_int, C.c_double, C.c_int, dp, dp, ip,
+        L.lyap_ir_solve.argtypes = [vp, dp, dp, C.c_int, dp, C.c_int, C.c_int, C.c_double, C.c_int, dp, dp, ip,
                                     C.POINTER(Report)]
         L.lyap_ir_solve_host.argtypes = L.lyap_ir_solve.argtypes
         L.lyap_invert.argtypes = [C.c_int, C.c_int, vp, vp, vp]
@@ -214,8 +215,9 @@ class Solver:
             pass
 
     # ---- full IR solve (device buffers)
-    def solve(self, A, Lt, S=None, tol=1e-14, maxit=50, out=None) -> Result:
-        """A: (n,n) fp64 CUDA; Lt: (m,n) fp64 CUDA (= L^T); S: (m,m) fp64 CUDA or None."""
+    def solve(self, A, Lt, S=None, tol=1e-14, maxit=50, out=None, us=None) -> Result:
+        """A: (n,n) fp64 CUDA; Lt: (m,n) fp64 CUDA (= L^T); S: (m,m) fp64 CUDA or None;
+        us: solver precision for this solve (None: the handle's current one)."""
         import torch
         n, cm = self.n, self.max_cols
         m = Lt.shape[0] if isinstance(Lt, torch.Tensor) and Lt.dim() == 2 else -1
@@ -230,14 +232,16 @@ class Solver:
             Zt, Yb = out
         rank = C.c_int(0)
         rep = Report()
-        _check(lib().lyap_ir_solve(self.h, _ptr(A), _ptr(Lt), m, _ptr(S), FP64, tol, maxit, _ptr(Zt),
+        if us is not None:
+            self.us = _prec(us)
+        _check(lib().lyap_ir_solve(self.h, _ptr(A), _ptr(Lt), m, _ptr(S), self.us, FP64, tol, maxit, _ptr(Zt),
                                    _ptr(Yb), C.byref(rank), C.byref(rep)), "lyap_ir_solve")
         r = rank.value
         Y = Yb[:r, :r] if Yb is not None else None      # Yb is column-major cm x cm: Y[i,j] = Yb[j,i]
         return Result(Z=Zt[:r].T, Y=(Y.T if Y is not None else None), report=rep.as_dict())
 
     # ---- end-to-end with host (numpy) buffers
-    def solve_host(self, A, Lt, S=None, tol=1e-14, maxit=50):
+    def solve_host(self, A, Lt, S=None, tol=1e-14, maxit=50, us=None):
         import numpy as np
         n, cm = self.n, self.max_cols
         A = np.ascontiguousarray(A, dtype=np.float64)
@@ -252,7 +256,9 @@ class Solver:
         rank = C.c_int(0)
         rep = Report()
         p = lambda a: None if a is None else a.ctypes.data
-        _check(lib().lyap_ir_solve_host(self.h, p(A), p(Lt), Lt.shape[0], p(S), FP64, tol, maxit, p(Zt),
+        if us is not None:
+            self.us = _prec(us)
+        _check(lib().lyap_ir_solve_host(self.h, p(A), p(Lt), Lt.shape[0], p(S), self.us, FP64, tol, maxit, p(Zt),
                                         p(Yb), C.byref(rank), C.byref(rep)), "lyap_ir_solve_host")
         r = rank.value
         return Zt[:r].T, (Yb[:r, :r].T if Yb is not None else None), rep.as_dict()

@@ -228,6 +228,102 @@ dgemm_dmma_kernel(int M, int N, int K, int kchunk, double alpha,
               scm, scn, work, (long)blockIdx.z * M * N);
 }
 
+
+// ---------------------------------------------------------------- fp32 SIMT, 128 x 128 tiles
+// C = alpha A B^T + beta C for fp32 with both operands K-contiguous (A(i,l) = A[i sam + l],
+// B(l,j) = B[l + j sbn]) -- the shapes of the fp32 solver's Gauss-Jordan update and of its
+// A_k^{-1} Z products.  256 threads, 8 x 8 outputs per thread, BK = 16 k-slices staged
+// transposed in shared memory (double-buffered through registers, 16-byte loads when the
+// rows are 16-byte aligned); split-K partials go to `work` like gemm_strided_kernel.
+constexpr int SG_BM = 128, SG_BN = 128, SG_BK = 16;
+static __global__ void __launch_bounds__(256)
+sgemm_nt_kernel(int M, int N, int K, int kchunk, float alpha, const float *__restrict__ A, long sam,
+                const float *__restrict__ B, long sbn, float beta, float *__restrict__ C, long scm, long scn,
+                float *__restrict__ work, int vec)
+{
+    __shared__ __align__(16) float As[2][SG_BK][SG_BM + 4];
+    __shared__ __align__(16) float Bs[2][SG_BK][SG_BN + 4];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const long m0 = (long)blockIdx.y * SG_BM, n0 = (long)blockIdx.x * SG_BN;
+    const int kb = blockIdx.z * kchunk, ke = min(K, kb + kchunk);
+    // loader: thread -> (row r = tid / 4 + 64 h, k quad q = tid % 4), h = 0, 1
+    const int lr = tid >> 2, lq = (tid & 3) * 4;
+    float ra[2][4], rb[2][4];
+    auto gload = [&](int k0) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const long gm = m0 + lr + 64 * h, gn = n0 + lr + 64 * h;
+            const int gk = k0 + lq;
+            if (vec && gk + 4 <= ke) {
+                float4 a4 = (gm < M) ? *reinterpret_cast<const float4 *>(A + gm * sam + gk) : make_float4(0.f, 0.f, 0.f, 0.f);
+                float4 b4 = (gn < N) ? *reinterpret_cast<const float4 *>(B + gn * sbn + gk) : make_float4(0.f, 0.f, 0.f, 0.f);
+                ra[h][0] = a4.x; ra[h][1] = a4.y; ra[h][2] = a4.z; ra[h][3] = a4.w;
+                rb[h][0] = b4.x; rb[h][1] = b4.y; rb[h][2] = b4.z; rb[h][3] = b4.w;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    ra[h][e] = (gm < M && gk + e < ke) ? A[gm * sam + gk + e] : 0.f;
+                    rb[h][e] = (gn < N && gk + e < ke) ? B[gn * sbn + gk + e] : 0.f;
+                }
+            }
+        }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+        for (int h = 0; h < 2; h++)
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                As[buf][lq + e][lr + 64 * h] = ra[h][e];
+                Bs[buf][lq + e][lr + 64 * h] = rb[h][e];
+            }
+    };
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+#pragma unroll
+        for (int j = 0; j < 8; j++) acc[i][j] = 0.f;
+    const int ntiles = (ke > kb) ? (ke - kb + SG_BK - 1) / SG_BK : 0;
+    if (ntiles > 0) { gload(kb); sstore(0); }
+    __syncthreads();
+    for (int t = 0; t < ntiles; t++) {
+        const int buf = t & 1;
+        if (t + 1 < ntiles) gload(kb + (t + 1) * SG_BK);
+#pragma unroll
+        for (int kk = 0; kk < SG_BK; kk++) {
+            // rows ty*4 + {0..3} and 64 + ty*4 + {0..3}; columns likewise (conflict-free float4)
+            const float4 a0 = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * 4]);
+            const float4 a1 = *reinterpret_cast<const float4 *>(&As[buf][kk][64 + ty * 4]);
+            const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][tx * 4]);
+            const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][64 + tx * 4]);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int j = 0; j < 8; j++) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        if (t + 1 < ntiles) sstore(buf ^ 1);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const long gm = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        if (gm >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const long gn = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+            if (gn >= N) continue;
+            const float r = alpha * acc[i][j];
+            if (work) {
+                work[(long)blockIdx.z * M * N + gm + gn * (long)M] = r;
+            } else {
+                float *cp = C + gm * scm + gn * scn;
+                *cp = (beta != 0.f) ? fmaf(beta, *cp, r) : r;
+            }
+        }
+    }
+}
+
 template <typename TA, typename TB, typename TC, typename Acc>
 int gemm_strided(cudaStream_t s, int M, int N, int K, Acc alpha,
                  const TA *A, long sam, long sak, const TB *B, long sbk, long sbn,
@@ -252,6 +348,31 @@ int gemm_strided(cudaStream_t s, int M, int N, int K, Acc alpha,
     const int kchunk = (splits > 1) ? ceil_div(ceil_div(K, splits), BK) * BK : std::max(K, 1);
     if (splits > 1) splits = ceil_div(K, kchunk);
     dim3 grid(ceil_div(N, BN), ceil_div(M, BM), splits);
+    constexpr bool all_f32 = std::is_same<TA, float>::value && std::is_same<TB, float>::value &&
+                             std::is_same<TC, float>::value && std::is_same<Acc, float>::value;
+    if constexpr (all_f32) {
+        // 128 x 128 tiles for K-contiguous operands (both fp32 solver shapes) with enough tiles
+        const long tiles128 = (long)ceil_div(N, SG_BN) * ceil_div(M, SG_BM);
+        if (sak == 1 && sbk == 1 && tiles128 >= 64 && !env_flag("LYAP_SGEMM_OLD")) {
+            int sp = 1;
+            if (tiles128 < 148 && K >= 512) sp = std::min(std::min(ceil_div(K, 256), std::max(1, (int)(296 / tiles128))), 64);
+            float *wk = nullptr;
+            if (sp > 1) { wk = (float *)splitk_workspace(sizeof(float) * (size_t)sp * M * N, s); if (!wk) sp = 1; }
+            const int kc = (sp > 1) ? ceil_div(ceil_div(K, sp), SG_BK) * SG_BK : std::max(K, 1);
+            if (sp > 1) sp = ceil_div(K, kc);
+            const int vec = (sam % 4 == 0 && sbn % 4 == 0 && ((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0) ? 1 : 0;
+            dim3 g2(ceil_div(N, SG_BN), ceil_div(M, SG_BM), sp);
+            sgemm_nt_kernel<<<g2, 256, 0, s>>>(M, N, K, kc, alpha, A, sam, B, sbn, beta, C, scm, scn,
+                                               sp > 1 ? wk : nullptr, vec);
+            LYAP_TRY(launched());
+            if (sp > 1) {
+                int gr = std::min(ceil_div((long)M * N, 256), 2048);
+                splitk_reduce_kernel<TC, Acc><<<gr, 256, 0, s>>>(M, N, sp, wk, beta, C, scm, scn);
+                LYAP_TRY(launched());
+            }
+            return LYAP_OK;
+        }
+    }
     if constexpr (all_f64) {
         KTimer kt(KC_DGEMM, s, 2.0 * M * N * K, 8.0 * ((double)M * K + (double)K * N + 2.0 * M * N));
         dgemm_dmma_kernel<<<grid, 128, 0, s>>>(M, N, K, kchunk, alpha, A, sam, sak, B, sbk, sbn, beta, C, scm,

@@ -37,7 +37,8 @@ template <typename T>
 __global__ void __launch_bounds__(1024)
 gje_panel_kernel(int n, int k, int b, T *__restrict__ A, T *__restrict__ X,
                  int *__restrict__ ipiv, int *__restrict__ moved, int *__restrict__ nmoved,
-                 int *__restrict__ info, typename Prec<T>::acc *__restrict__ Pglob, int use_smem)
+                 int *__restrict__ info, typename Prec<T>::acc *__restrict__ Pglob, int use_smem,
+                 double *__restrict__ ldet)
 {
     using Acc = typename Prec<T>::acc;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -159,6 +160,10 @@ gje_panel_kernel(int n, int k, int b, T *__restrict__ A, T *__restrict__ X,
     // ---- pivots and the list of moved rows (dst local pos, src local row)
     if (tid == 0) {
         for (int j = 0; j < b; j++) ipiv[k + j] = k + pivl[j];
+        // log|det| contribution of this panel: the Gauss-Jordan pivots are U's diagonal
+        double sl = 0.0;
+        for (int j = 0; j < b; j++) sl += log(fabs((double)P[(long)j * b + j]));
+        ldet[k] = sl;
         if (*sflag && *info == 0) *info = *sflag;
         // replay the transpositions on a small position map of candidates
         int cand[64], src[64], nc = 0;
@@ -315,7 +320,7 @@ __global__ void __launch_bounds__(NT)
 gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T *__restrict__ X,
                          int *__restrict__ ipiv, int *__restrict__ moved, int *__restrict__ nmoved,
                          int *__restrict__ info, typename Prec<T>::acc *__restrict__ Tglob,
-                         typename Prec<T>::acc *__restrict__ Pg)
+                         typename Prec<T>::acc *__restrict__ Pg, double *__restrict__ ldet)
 {
     namespace cg = cooperative_groups;
     using Acc = typename Prec<T>::acc;
@@ -529,6 +534,9 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
                 *nmoved = mm;
                 for (int j = 0; j < b; j++) ipiv[k + j] = k + pivl[j];
                 if (sflag && *info == 0) *info = sflag;
+                double sl = 0.0;                 // log|det| contribution (U's diagonal)
+                for (int j = 0; j < b; j++) sl += log(fabs((double)Ptop[j][j]));
+                ldet[k] = sl;
             }
         }
         __syncthreads();
@@ -778,6 +786,7 @@ int GjeWork::alloc(int n_, int prec_) {
         omoved = oints; onmoved = oints + 4 * GJE_NB; slot_of = onmoved + 4; invprev = slot_of + GJE_NB;
     }
     LYAP_CUDA_TRY(cudaMalloc(&ints, sizeof(int) * (size_t)(4 * n + 4 * b + 8)));
+    LYAP_CUDA_TRY(cudaMalloc(&ldet, sizeof(double) * (size_t)n));
     ipiv = ints; rowperm = ipiv + n; invperm = rowperm + n; moved = invperm + n;
     nmoved = moved + 4 * b; info = nmoved + 1; tmp_perm = info + 1;
     return LYAP_OK;
@@ -785,7 +794,7 @@ int GjeWork::alloc(int n_, int prec_) {
 
 void GjeWork::release() {
     cudaFree(X); cudaFree(B); cudaFree(tmp); cudaFree(Pglob); cudaFree(Tg); cudaFree(Bo); cudaFree(tmp2);
-    cudaFree(ints); cudaFree(oints);
+    cudaFree(ints); cudaFree(oints); cudaFree(ldet);
     if (side) { cudaStreamSynchronize(side); cudaStreamDestroy(side); side = nullptr; }
     if (ev_a) { cudaEventDestroy(ev_a); ev_a = nullptr; }
     if (ev_b) { cudaEventDestroy(ev_b); ev_b = nullptr; }
@@ -890,10 +899,10 @@ static int gje_panel_launch(cudaStream_t s, int n, int k, int b, T *A, GjeWork &
         }();
         (void)attr1;
         gje_panel_kernel<T><<<1, 1024, sm, s>>>(n, k, b, A, (T *)w.X, w.ipiv, w.moved, w.nmoved, w.info,
-                                                (Acc *)w.Pglob, use_smem ? 1 : 0);
+                                                (Acc *)w.Pglob, use_smem ? 1 : 0, w.ldet);
         return launched();
     }
-    void (*kern)(int, int, int, int, const T *, T *, int *, int *, int *, int *, Acc *, Acc *);
+    void (*kern)(int, int, int, int, const T *, T *, int *, int *, int *, int *, Acc *, Acc *, double *);
     if (NTh == 1024) kern = (RB > 1024) ? gje_panel_cluster_kernel<T, BW, 2, 1024> : gje_panel_cluster_kernel<T, BW, 1, 1024>;
     else kern = (RB > 512) ? gje_panel_cluster_kernel<T, BW, 2, 512> : gje_panel_cluster_kernel<T, BW, 1, 512>;
     // one-time setup (function-local static: thread-safe initialisation)
@@ -918,7 +927,7 @@ static int gje_panel_launch(cudaStream_t s, int n, int k, int b, T *A, GjeWork &
     cfg.attrs = at;
     cfg.numAttrs = 1;
     LYAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, n, k, b, RB, (const T *)A, (T *)w.X, w.ipiv, w.moved, w.nmoved,
-                                     w.info, (Acc *)w.Tg, (Acc *)w.Pglob));
+                                     w.info, (Acc *)w.Tg, (Acc *)w.Pglob, w.ldet));
     LYAP_TRY(launched());
     const int rows = k + std::max(0, R - b);                 // above the panel + below the block
     if (rows > 0)
@@ -933,6 +942,7 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
     using Acc = typename Prec<T>::acc;
     const int b0 = gje_panel_width(Prec<T>::code);
     LYAP_CUDA_TRY(cudaMemsetAsync(w.info, 0, sizeof(int), s));
+    LYAP_CUDA_TRY(cudaMemsetAsync(w.ldet, 0, sizeof(double) * (size_t)n, s));
     iota_kernel<<<ceil_div(n, 256), 256, 0, s>>>(n, w.rowperm);
     LYAP_TRY(launched());
     // two-level blocking for the 16-bit types: inner 32-wide steps restricted to an

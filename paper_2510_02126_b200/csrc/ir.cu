@@ -136,7 +136,10 @@ int aseq_compute(lyap_ir_ctx *h, const double *A) {
         }
         LYAP_TRY(nk_scale(s, us, nn, h->Ak, h->W, h->scal));
         LYAP_TRY(gje_invert(s, n, us, h->W, h->gje));
-        LYAP_TRY(nk_mu(s, us, n, h->W, h->part, h->scal, scaling_on));
+        // mu_k: Frobenius-norm scaling (opt.scaling = 1, the paper's choice l.1406) or
+        // determinantal scaling |det A_k|^{-1/n} (opt.scaling = 2, l.1139)
+        if (h->opt.scaling == 2) LYAP_TRY(nk_mu_det(s, n, h->gje.ldet, h->scal, scaling_on));
+        else LYAP_TRY(nk_mu(s, us, n, h->W, h->part, h->scal, scaling_on));
         LYAP_TRY(nk_update(s, us, n, h->Ak, h->W, h->gje.invperm, h->An, h->inv[it - 1], h->scal, h->part));
         LYAP_TRY(nk_roll(s, h->scal));
         int info = 0;
@@ -436,6 +439,30 @@ int implied_norm2(lyap_ir_ctx *h, int c, const double *Z, const double *Y, int l
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) { float ms = 0.f; cudaEventElapsedTime(&ms, a, b); return ms; }
 
+// Solver precision u_s per solve (the paper's problem statement passes u_s with the
+// equation): a different u_s than the handle's current one re-allocates the u_s-typed
+// buffers (A_k, A_{k+1}, W, Z_k, the Gauss-Jordan workspace) and drops the inverse cache.
+int set_precision(lyap_ir_ctx *h, int us) {
+    if (us < 0 || us == h->us) return LYAP_OK;
+    if (us > 3) return LYAP_ERR_ARG;
+    LYAP_CUDA_TRY(cudaStreamSynchronize(h->s));
+    for (void *p : {h->Ak, h->An, h->W, h->Zt}) cudaFree(p);
+    for (void *p : h->inv) cudaFree(p);
+    h->inv.clear();
+    h->ksteps = 0;
+    h->Ak = h->An = h->W = h->Zt = nullptr;
+    h->gje.release();
+    h->gje = GjeWork();
+    h->us = us;
+    h->es = elem_size(us);
+    const size_t nn = (size_t)h->n * h->n;
+    LYAP_TRY(dmalloc(&h->Ak, h->es * nn));
+    LYAP_TRY(dmalloc(&h->An, h->es * nn));
+    LYAP_TRY(dmalloc(&h->W, h->es * nn));
+    LYAP_TRY(dmalloc(&h->Zt, h->es * (size_t)h->n * h->PZ));
+    return h->gje.alloc(h->n, us);
+}
+
 int ir_solve(lyap_ir_ctx *h, const double *A, const double *L, int m, const double *S, int ur, double tol,
              int maxit, double *Zout, double *Yout, int *rank_out, lyap_ir_report *rep) {
     const int n = h->n;
@@ -588,6 +615,8 @@ void lyap_ir_default_options(lyap_ir_options *o) {
     o->eta_r = 1e-4;
     o->eta_s = 10.0 * 0x1p-53;
     o->cache = 1;
+    o->newton_cols = 0;
+    o->work_cols = 0;
 }
 
 int64_t lyap_launch_count(void) { return g_launches.load(); }
@@ -603,8 +632,8 @@ int lyap_ir_create(lyap_ir_handle *out, int n, int cmax, int us, const lyap_ir_o
     h->es = elem_size(us);
     const int rho_n = (int)std::ceil(h->opt.rho * n);
     h->PF = 2 * cmax + h->mmax;
-    h->PZ = 2 * std::max(h->PF, rho_n) + 16;
-    h->PW = h->PF + h->PZ;
+    h->PZ = h->opt.newton_cols > 0 ? h->opt.newton_cols : 2 * std::max(h->PF, rho_n) + 16;
+    h->PW = h->opt.work_cols > 0 ? std::max(h->opt.work_cols, h->PF) : h->PF + h->PZ;
     const size_t nn = (size_t)n * n;
     int rc = LYAP_OK;
     auto A = [&](int r) { if (rc == LYAP_OK) rc = r; };
@@ -664,15 +693,17 @@ int lyap_ir_destroy(lyap_ir_handle h) {
     return LYAP_OK;
 }
 
-int lyap_ir_solve(lyap_ir_handle h, const double *A, const double *L, int m, const double *S, int ur, double tol,
-                  int maxit, double *Z, double *Y, int *rank, lyap_ir_report *rep) {
-    if (!h || !A || !L || !Z || !rank) return LYAP_ERR_ARG;
+int lyap_ir_solve(lyap_ir_handle h, const double *A, const double *L, int m, const double *S, int us, int ur,
+                  double tol, int maxit, double *Z, double *Y, int *rank, lyap_ir_report *rep) {
+    if (!h || !A || !L || !Z || !rank || us > 3) return LYAP_ERR_ARG;
+    LYAP_TRY(set_precision(h, us));
     return ir_solve(h, A, L, m, S, ur, tol, maxit, Z, Y, rank, rep);
 }
 
-int lyap_ir_solve_host(lyap_ir_handle h, const double *A, const double *L, int m, const double *S, int ur,
-                       double tol, int maxit, double *Z, double *Y, int *rank, lyap_ir_report *rep) {
-    if (!h || !A || !L || !Z || !rank || m <= 0 || m > h->mmax) return LYAP_ERR_ARG;
+int lyap_ir_solve_host(lyap_ir_handle h, const double *A, const double *L, int m, const double *S, int us,
+                       int ur, double tol, int maxit, double *Z, double *Y, int *rank, lyap_ir_report *rep) {
+    if (!h || !A || !L || !Z || !rank || m <= 0 || m > h->mmax || us > 3) return LYAP_ERR_ARG;
+    LYAP_TRY(set_precision(h, us));
     const int n = h->n;
     if (!h->hA) {
         LYAP_TRY(dalloc(&h->hA, (size_t)n * n));

@@ -16,6 +16,7 @@ struct GjeWork {
     int *ints = nullptr;
     int *ipiv = nullptr, *rowperm = nullptr, *invperm = nullptr, *moved = nullptr;
     int *nmoved = nullptr, *info = nullptr, *tmp_perm = nullptr;
+    double *ldet = nullptr;               // log|pivot| sums per panel start (log|det| of the matrix)
     int alloc(int n, int prec);
     void release();
 };
@@ -52,6 +53,8 @@ struct SyevdWork {
     int pmax = 0;
     double *A = nullptr, *Q = nullptr, *Qg = nullptr, *Qk = nullptr, *U = nullptr, *Qn = nullptr, *R = nullptr;
     double *vec = nullptr, *rot = nullptr;
+    double *gvec = nullptr;      // tridiagonalisation vectors in global memory (p > 6400)
+    int gvec_ctas = 0;
     int *ivec = nullptr;
     int alloc(int pmax);
     void release();
@@ -75,6 +78,10 @@ struct RrqrWork {
     int nmax = 0, cmax = 0;
     double *M = nullptr, *nrm = nullptr, *scal = nullptr;
     int *ints = nullptr;
+    // blocked QRCP: reflectors (cmax x 32), F (nmax x 32), partials, state
+    double *V3 = nullptr, *F3 = nullptr, *p3 = nullptr, *st3 = nullptr;
+    int *act3 = nullptr, *ist3 = nullptr;
+    int p3_ctas = 0;
     int alloc(int nmax, int cmax);
     void release();
 };

@@ -176,6 +176,25 @@ __global__ void mu_kernel(int scaling, double *scal)
     scal[SC_MU] = mu;
 }
 
+// Determinantal scaling mu_k = |det A_k|^{-1/n}: the inversion leaves
+// log|u_jj| summed per panel in ldet (zeros elsewhere); W = 2^{-e} A_k was inverted, so
+// log|det A_k| = log|det W| + n e ln 2.  One CTA, fixed reduction order.
+__global__ void __launch_bounds__(256) mu_det_kernel(int n, int scaling, const double *__restrict__ ldet, double *scal)
+{
+    __shared__ double red[32];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) t += ldet[i];
+    t = block_sum(t, red);
+    if (threadIdx.x == 0) {
+        const double e = scal[SC_EXP];
+        const double ld = t + (double)n * e * 0.69314718055994530942;
+        double mu = 1.0;
+        if (scaling && isfinite(ld)) mu = exp(-ld / (double)n);
+        if (!(mu > 0.0) || !isfinite(mu)) mu = 1.0;
+        scal[SC_MU] = mu;
+    }
+}
+
 // A_{k+1} = 0.5 (mu A_k + mu^{-1} A_k^{-1}),  A_k^{-1}[i][j] = 2^{-e} G[i][invperm[j]].
 template <typename T>
 __global__ void __launch_bounds__(256)
@@ -571,6 +590,12 @@ int nk_mu(cudaStream_t s, int prec, int n, const void *G, double *part, double *
     reduce_rows_kernel<<<1, 1024, 0, s>>>(n, part, scal + SC_RED);
     LYAP_TRY(launched());
     mu_kernel<<<1, 1, 0, s>>>(scaling, scal);
+    return launched();
+}
+
+int nk_mu_det(cudaStream_t s, int n, const double *ldet, double *scal, int scaling)
+{
+    mu_det_kernel<<<1, 256, 0, s>>>(n, scaling, ldet, scal);
     return launched();
 }
 

@@ -24,6 +24,7 @@ enum {
 int nk_cast(cudaStream_t s, int prec, int n, const double *A, void *Ak, double *part, double *out);
 int nk_scale(cudaStream_t s, int prec, long nn, const void *Ak, void *W, double *scal);
 int nk_mu(cudaStream_t s, int prec, int n, const void *G, double *part, double *scal, int scaling);
+int nk_mu_det(cudaStream_t s, int n, const double *ldet, double *scal, int scaling);
 int nk_update(cudaStream_t s, int prec, int n, const void *Ak, const void *G, const int *invperm, void *Anext,
               void *Ainv, double *scal, double *part);
 int nk_roll(cudaStream_t s, double *scal);

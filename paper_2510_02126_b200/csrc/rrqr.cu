@@ -12,6 +12,7 @@
 // Grid-wide barriers separate the phases.
 #include <cooperative_groups.h>
 #include "common.cuh"
+#include "gemm_simt.cuh"
 #include "lyap_internal.h"
 #include "ktimer.h"
 
@@ -361,6 +362,203 @@ rrqr2_kernel(Rrqr2Args a)
 #endif
 }
 
+
+// ---------------------------------------------------------------------------------
+// Blocked QRCP (LAPACK xLAQPS scheme).  Same pivots and
+// reflectors as rrqr2 (up to rounding), but within a block of RQ_NB steps the trailing
+// matrix is not updated: step j (= j0 + jj) forms
+//   u   = M[j0:, pc] - V[j0:, 0:jj] F[pc, 0:jj]^T         (the pivot column, updated)
+//   v, tau from u[j:]                                        (reflector H_j)
+//   F[col, jj] = tau (M[j:, col]^T v - F[col, 0:jj] (V[j:, 0:jj]^T v))   (read-only GEMV)
+//   M[j, col] -= V[j, 0:jj+1] F[col, 0:jj+1]^T              (row j of R, final)
+// and downdates the trailing norms with row j.  A block ends after RQ_NB steps, or early
+// after a step whose downdate cancelled (the xLAQP2 sqrt(eps) rule); then one DMMA GEMM
+// applies the block to the trailing rows, M[j0+nb:, :] -= V[j0+nb:, :] F^T, and the next
+// launch recomputes every trailing norm exactly.  Per step the trailing matrix is read
+// once and not written (rrqr2: read and written); one grid barrier per step.
+constexpr int RQ_NB = 32;
+struct Rrqr3Args {
+    int n, c, kmax, j0;
+    double tol;
+    double *M;          // c x n col-major
+    double *V;          // c x RQ_NB col-major (reflectors of this block, zero above their row)
+    double *F;          // n x RQ_NB, row col at F + col * RQ_NB
+    double *bsum, *bbest; int *bidx, *bflag;   // 2 x gridDim partials (step parity)
+    int *perm;          // n: pivot order
+    int *active;        // n: 1 while not pivoted
+    double *state;      // [0] r11
+    int *istate;        // [0] next j, [1] done (rank final), [2] rank
+};
+
+__global__ void __launch_bounds__(256, 2)
+rrqr3_kernel(Rrqr3Args a)
+{
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double rq_sm[];
+    double *ush = rq_sm;                     // c: updated pivot column -> reflector v (rows j..)
+    __shared__ double wv[RQ_NB];             // V[j:, 0:jj]^T v
+    __shared__ double red[32];
+    __shared__ double s_best[8], s_sum[8];
+    __shared__ int s_idx[8], s_flag[8];
+    __shared__ double s_t;
+    __shared__ int s_bi, s_fl;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const int gw = blockIdx.x * nwb + wib, nwg = gridDim.x * nwb;
+    const int n = a.n, c = a.c, G = gridDim.x, j0 = a.j0;
+    double r11 = (j0 > 0) ? a.state[0] : 0.0;
+    // owned columns col = gw + t nwg: lane t keeps the trailing norm^2, its value at the
+    // block start (exact), and the active flag
+    double m_n2 = 0.0, m_n0 = 0.0;
+    bool m_act = false;
+    auto publish = [&](int buf, double bsum, double bbest, int bidx, int flag) {
+        if (lane == 0) { s_sum[wib] = bsum; s_best[wib] = bbest; s_idx[wib] = bidx; s_flag[wib] = flag; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0, bv = -1.0; int bi = n, fl = 0;
+            for (int w = 0; w < nwb; w++) {
+                t += s_sum[w]; fl |= s_flag[w];
+                if (s_best[w] > bv || (s_best[w] == bv && s_idx[w] < bi)) { bv = s_best[w]; bi = s_idx[w]; }
+            }
+            a.bsum[buf * G + blockIdx.x] = t; a.bbest[buf * G + blockIdx.x] = bv;
+            a.bidx[buf * G + blockIdx.x] = bi; a.bflag[buf * G + blockIdx.x] = fl;
+        }
+    };
+    {   // exact trailing norms (rows j0..c-1) of the active columns
+        double bsum = 0.0, bbest = -1.0; int bidx = n;
+        for (int col = gw, t = 0; col < n; col += nwg, t++) {
+            const bool act = a.active[col] != 0;
+            double sq = 0.0;
+            if (act) {
+                const double *x = a.M + (long)col * c;
+#pragma unroll 8
+                for (int i = j0 + lane; i < c; i += 32) sq = fma(x[i], x[i], sq);
+                sq = warp_sum(sq);
+                bsum += sq;
+                if (sq > bbest || (sq == bbest && col < bidx)) { bbest = sq; bidx = col; }
+            }
+            if (lane == t) { m_n2 = sq; m_n0 = sq; m_act = act; }
+        }
+        publish(0, bsum, bbest, bidx, 0);
+    }
+    int prev = -1, jj = 0, stopped = 0;
+    double prev_alpha = 0.0;
+    for (; jj < RQ_NB && j0 + jj < a.kmax; jj++) {
+        const int j = j0 + jj;
+        grid.sync();
+        const int buf = jj & 1;
+        if (wib == 0) {
+            double t = 0.0, bv = -1.0; int bi = n, fl = 0;
+            for (int b = lane; b < G; b += 32) {
+                t += a.bsum[buf * G + b]; fl |= a.bflag[buf * G + b];
+                const double v = a.bbest[buf * G + b]; const int i2 = a.bidx[buf * G + b];
+                if (v > bv || (v == bv && i2 < bi)) { bv = v; bi = i2; }
+            }
+            t = warp_sum(t);
+            fl = __reduce_or_sync(0xffffffffu, fl);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; }
+            }
+            if (lane == 0) { s_t = t; s_bi = bi; s_fl = fl; }
+        }
+        __syncthreads();
+        const double tr = sqrt(s_t);
+        const int bi = s_bi;
+        // owners finalise the previous pivot column (every CTA has finished reading it)
+        if (prev >= 0 && (prev % nwg) == gw) {
+            double *xp = a.M + (long)prev * c;
+            for (int i = j - 1 + lane; i < c; i += 32) xp[i] = (i == j - 1) ? prev_alpha : 0.0;
+            if (lane < RQ_NB) a.F[(long)prev * RQ_NB + lane] = 0.0;
+        }
+        if (s_fl) break;                     // a downdate cancelled in the previous step: end the block
+        if ((j > 0 && tr <= a.tol * r11) || tr == 0.0 || bi >= n) { stopped = 1; break; }
+        const int pc = bi;
+        // ---- u = M[j0:, pc] - V[j0:, 0:jj] F[pc, 0:jj]^T; reflector from u[j:]
+        const double *xp = a.M + (long)pc * c;
+        const double *Fp = a.F + (long)pc * RQ_NB;
+        double part = 0.0;
+        for (int i = j + threadIdx.x; i < c; i += blockDim.x) {
+            double x = xp[i];
+            for (int l = 0; l < jj; l++) x = fma(-a.V[(long)l * c + i], Fp[l], x);
+            ush[i] = x;
+            if (i > j) part = fma(x, x, part);
+        }
+        part = block_sum(part, red);
+        const double x0 = ush[j];
+        const double nrm = sqrt(part + x0 * x0);
+        const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+        const double v0 = x0 - alpha;
+        const double vtv = v0 * v0 + part;
+        const double tau = (vtv != 0.0) ? 2.0 / vtv : 0.0;
+        __syncthreads();
+        if (threadIdx.x == 0) ush[j] = v0;
+        if (j == 0) r11 = fabs(alpha);
+        __syncthreads();
+        // w = V[j:, 0:jj]^T v (warp l handles l, l + 8, ...)
+        for (int l = wib; l < jj; l += nwb) {
+            double d = 0.0;
+            for (int i = j + lane; i < c; i += 32) d = fma(a.V[(long)l * c + i], ush[i], d);
+            d = warp_sum(d);
+            if (lane == 0) wv[l] = d;
+        }
+        if (blockIdx.x == 0) {
+            for (int i = threadIdx.x; i < c; i += blockDim.x) a.V[(long)jj * c + i] = (i >= j) ? ush[i] : 0.0;
+            if (threadIdx.x == 0) {
+                a.perm[j] = pc; a.active[pc] = 0;
+                if (j == 0) a.state[0] = fabs(alpha);
+            }
+        }
+        __syncthreads();
+        // ---- owners: F[col, jj], row j of R, norm downdate, next partials
+        double bsum = 0.0, bbest = -1.0; int bidx = n, flag = 0;
+        const double vj = (lane <= jj) ? ((lane == jj) ? v0 : a.V[(long)lane * c + j]) : 0.0;   // V[j, lane]
+        const double wl = (lane < jj) ? wv[lane] : 0.0;
+        for (int col = gw, t = 0; col < n; col += nwg, t++) {
+            if (col == pc) { if (lane == t) m_act = false; continue; }
+            if (!__shfl_sync(0xffffffffu, (int)m_act, t)) continue;
+            const double *y = a.M + (long)col * c;
+            double d = 0.0;
+#pragma unroll 8
+            for (int i = j + lane; i < c; i += 32) d = fma(y[i], ush[i], d);
+            double *Fc = a.F + (long)col * RQ_NB;
+            const double fl = (lane < jj) ? Fc[lane] : 0.0;
+            const double corr = warp_sum(fl * wl);
+            d = warp_sum(d);
+            const double fnew = tau * (d - corr);
+            const double fall = (lane == jj) ? fnew : fl;
+            const double rj = y[j] - warp_sum(vj * fall);
+            if (lane == 0) { Fc[jj] = fnew; a.M[(long)col * c + j] = rj; }
+            double s2 = __shfl_sync(0xffffffffu, m_n2, t);
+            const double n0 = __shfl_sync(0xffffffffu, m_n0, t);
+            const double r = (s2 > 0.0) ? 1.0 - (rj * rj) / s2 : 0.0;
+            const double temp2 = fmax(r, 0.0) * (s2 / fmax(n0, 1e-300));
+            if (temp2 <= 1.5e-8) flag = 1;   // recomputed exactly at the next block start
+            s2 = fmax(s2 - rj * rj, 0.0);
+            if (lane == t) m_n2 = s2;
+            bsum += s2;
+            if (s2 > bbest || (s2 == bbest && col < bidx)) { bbest = s2; bidx = col; }
+        }
+        publish(buf ^ 1, bsum, bbest, bidx, flag);
+        prev = pc; prev_alpha = alpha;
+    }
+    // block end: finalise the last pivot column once every CTA has read it
+    grid.sync();
+    if (prev >= 0 && (prev % nwg) == gw) {
+        const int jl = j0 + jj;              // steps j0 .. jl-1 done; prev was pivot of step jl-1
+        double *xp = a.M + (long)prev * c;
+        for (int i = jl - 1 + lane; i < c; i += 32) xp[i] = (i == jl - 1) ? prev_alpha : 0.0;
+        if (lane < RQ_NB) a.F[(long)prev * RQ_NB + lane] = 0.0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const int jl = j0 + jj;
+        a.istate[0] = jl;
+        a.istate[1] = (stopped || jl >= a.kmax) ? 1 : 0;
+        a.istate[2] = jl;
+    }
+}
+
 // Zout(col, r) = M[col][r] for r < k, rounded to prec (physical columns = rows of Z)
 __global__ void rrqr2_out_kernel(int n, int c, int k, const double *__restrict__ M, int prec, double *__restrict__ Zout)
 {
@@ -399,9 +597,81 @@ int RrqrWork::alloc(int nmax_, int cmax_) {
     LYAP_CUDA_TRY(cudaMalloc(&nrm, sizeof(double) * (size_t)(2 * nmax + 4 * 1024 + cmax + 8)));
     LYAP_CUDA_TRY(cudaMalloc(&ints, sizeof(int) * (size_t)(2 * nmax + 2048 + 16)));
     scal = nrm + nmax;
+    p3_ctas = 512;
+    LYAP_CUDA_TRY(cudaMalloc(&V3, sizeof(double) * (size_t)cmax * RQ_NB));
+    LYAP_CUDA_TRY(cudaMalloc(&F3, sizeof(double) * (size_t)nmax * RQ_NB));
+    LYAP_CUDA_TRY(cudaMalloc(&p3, sizeof(double) * (size_t)8 * p3_ctas));
+    LYAP_CUDA_TRY(cudaMalloc(&st3, sizeof(double) * 4));
+    LYAP_CUDA_TRY(cudaMalloc(&act3, sizeof(int) * ((size_t)nmax + 8)));
+    ist3 = act3 + nmax;
     return LYAP_OK;
 }
-void RrqrWork::release() { cudaFree(M); cudaFree(nrm); cudaFree(ints); M = nrm = scal = nullptr; ints = nullptr; }
+void RrqrWork::release() {
+    for (double *p : {M, nrm, V3, F3, p3, st3}) if (p) cudaFree(p);
+    if (ints) cudaFree(ints);
+    if (act3) cudaFree(act3);
+    M = nrm = scal = V3 = F3 = p3 = st3 = nullptr;
+    ints = act3 = ist3 = nullptr;
+}
+
+__global__ void fill_int_kernel(int len, int v, int *x)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) x[i] = v;
+}
+
+// Blocked driver: one cooperative launch per block of RQ_NB pivots, then the block's
+// trailing update as one DMMA GEMM.  M = Z^T and perm are set up by the caller.
+static int rank_trunc_chol_blocked(cudaStream_t s, int n, int c, double tol, int prec_out, double *Zout,
+                                   int *k_out, RrqrWork &w)
+{
+    struct Cfg { int nsm, per; };
+    static const Cfg cfg = [] {
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(rrqr3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        return Cfg{nsm, 0};
+    }();
+    const size_t smem = sizeof(double) * (size_t)c;
+    if (smem > 200 * 1024) return LYAP_ERR_CAPACITY;
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr3_kernel, 256, smem);
+    const int grid = std::max(1, std::min(std::min(cfg.nsm * std::min(per, 2), w.p3_ctas), ceil_div(n, 8)));
+    if (n > 32 * 8 * grid) return LYAP_ERR_CAPACITY;
+    fill_int_kernel<<<std::min(ceil_div(n, 256), 1024), 256, 0, s>>>(n, 1, w.act3);
+    LYAP_TRY(launched());
+    const int kmax = c < n ? c : n;
+    int *ist = w.ist3;
+    int j0 = 0, k = 0;
+    int hs[3] = {0, 0, 0};
+    KTimer kt(KC_RRQR, s);
+    for (;;) {
+        Rrqr3Args a{n, c, kmax, j0, tol, w.M, w.V3, w.F3, w.p3, w.p3 + 2 * w.p3_ctas,
+                    (int *)(w.p3 + 4 * w.p3_ctas), (int *)(w.p3 + 4 * w.p3_ctas) + 2 * w.p3_ctas,
+                    w.ints, w.act3, w.st3, ist};
+        void *args[] = {&a};
+        LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)rrqr3_kernel, dim3(grid), dim3(256), args, smem, s));
+        LYAP_TRY(launched());
+        LYAP_CUDA_TRY(cudaMemcpyAsync(hs, ist, sizeof(int) * 3, cudaMemcpyDeviceToHost, s));
+        LYAP_CUDA_TRY(cudaStreamSynchronize(s));
+        if (hs[1]) { k = hs[2]; break; }
+        const int j1 = hs[0], nbb = j1 - j0;
+        if (nbb <= 0) return LYAP_ERR_CUDA;          // cannot happen: every launch makes a step or stops
+        if (j1 < c)
+            LYAP_TRY(dgemm_cm(s, false, false, c - j1, n, nbb, -1.0, w.V3 + j1, c, w.F3, RQ_NB, 1.0, w.M + j1, c));
+        j0 = j1;
+    }
+    if (k == 0) {   // all-zero Z: a single zero column (as the oracle)
+        LYAP_CUDA_TRY(cudaMemsetAsync(Zout, 0, sizeof(double) * (size_t)n, s));
+        *k_out = 1;
+        return LYAP_OK;
+    }
+    const long to = (long)n * k;
+    rrqr2_out_kernel<<<ceil_div(to, 256) < 2048 ? ceil_div(to, 256) : 2048, 256, 0, s>>>(n, c, k, w.M, prec_out, Zout);
+    LYAP_TRY(launched());
+    *k_out = k;
+    return LYAP_OK;
+}
 
 int rank_trunc_chol_f64(cudaStream_t s, int n, int c, const double *Z, double tol, int prec_out,
                         double *Zout, int *k_out, RrqrWork &w)
@@ -412,6 +682,11 @@ int rank_trunc_chol_f64(cudaStream_t s, int n, int c, const double *Z, double to
     long tot = (long)n * c;
     transpose_init_kernel<<<ceil_div(tot, 256) < 2048 ? ceil_div(tot, 256) : 2048, 256, 0, s>>>(n, c, Z, w.M, perm);
     LYAP_TRY(launched());
+    // blocked QRCP for factors that do not stay in L2 (the per-step GEMV reads the
+    // trailing matrix once instead of reading and writing it); LYAP_RRQR_BLOCKED=0/1 forces
+    const char *eb = getenv("LYAP_RRQR_BLOCKED");
+    const bool blocked = eb ? (eb[0] == '1') : ((double)n * c * 8.0 > 96e6);
+    if (blocked && w.V3) return rank_trunc_chol_blocked(s, n, c, tol, prec_out, Zout, k_out, w);
     const bool v2 = !env_flag("LYAP_RRQR_V1");
     // one-time setup (function-local static: thread-safe initialisation, published after
     // every attribute is set)

@@ -36,6 +36,8 @@ struct TridArgs {
     double *R;      // p x p col-major: reflector j in R[j+1:p, j] (R[j+1, j] = 1)
     double *d, *e, *tau;
     double *P;      // p
+    double *gvec;   // tridiag_kernel: per-CTA v, vn, w, c (4 p doubles each) in global memory
+                    // when 4 p doubles exceed shared memory (p > 6400); nullptr otherwise
 };
 
 // Reflector from x[0..L) (x[0] = alpha): v[0] = 1, v[i] = x[i]/(alpha - beta), tau, beta.
@@ -70,7 +72,8 @@ tridiag_kernel(TridArgs a)
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double sm[];
     const int p = a.p;
-    double *v = sm, *vn = sm + p, *w = sm + 2 * p, *c = sm + 3 * p;
+    double *vb = a.gvec ? a.gvec + (long)blockIdx.x * 4 * p : sm;
+    double *v = vb, *vn = vb + p, *w = vb + 2 * p, *c = vb + 3 * p;
     __shared__ double red[32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwb = blockDim.x >> 5;
     const int gw = blockIdx.x * nwb + wid, nwg = gridDim.x * nwb;
@@ -986,10 +989,15 @@ int SyevdWork::alloc(int pmax_) {
     LYAP_CUDA_TRY(cudaMalloc(&vec, sizeof(double) * (size_t)pmax * 16 + 32 * 33 * 64 * 8));
     LYAP_CUDA_TRY(cudaMalloc(&ivec, sizeof(int) * (size_t)pmax * 8 + 4096));
     LYAP_CUDA_TRY(cudaMalloc(&rot, sizeof(double) * (size_t)pmax * 4));
+    if (sizeof(double) * 4 * (size_t)pmax > 200 * 1024) {
+        gvec_ctas = 296;
+        LYAP_CUDA_TRY(cudaMalloc(&gvec, sizeof(double) * (size_t)gvec_ctas * 4 * pmax));
+    }
     return LYAP_OK;
 }
 void SyevdWork::release() {
-    for (double *b : {A, Q, Qg, Qk, U, Qn, R, vec, rot}) cudaFree(b);
+    for (double *b : {A, Q, Qg, Qk, U, Qn, R, vec, rot, gvec}) if (b) cudaFree(b);
+    gvec = nullptr;
     cudaFree(ivec);
     A = Q = Qg = Qk = U = Qn = R = vec = rot = nullptr;
     ivec = nullptr;
@@ -1020,9 +1028,10 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
     symmetrize_copy_kernel<<<gsz, 256, 0, s>>>(p, Ain, W.A);
     LYAP_TRY(launched());
     {
-        // shared memory for this p (the kernels address 4 p doubles), not the capacity
-        const size_t smem = sizeof(double) * 4 * (size_t)p;
-        if (smem > 200 * 1024) return LYAP_ERR_CAPACITY;
+        // shared memory for this p (the kernels address 4 p doubles), not the capacity;
+        // above 200 KB the general kernel keeps the four vectors in a global slice per CTA
+        const bool gvec = sizeof(double) * 4 * (size_t)p > 200 * 1024;
+        const size_t smem = gvec ? 0 : sizeof(double) * 4 * (size_t)p;
         // one-time attribute setup (function-local static: thread-safe initialisation)
         static const int nsm_t = [] {
             int dev = 0, v = 0;
@@ -1036,11 +1045,11 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
             return v;
         }();
         const int max_blocks = nsm_t;                 // one CTA per SM for the register-resident kernels
-        TridArgs ta{p, W.A, W.R, d, e, tau, P};
+        TridArgs ta{p, W.A, W.R, d, e, tau, P, gvec ? W.gvec : nullptr};
         void *args[] = {&ta};
         const int need = ceil_div(p, 8);             // one warp per column
         KTimer kt(KC_TRIDIAG, s, (4.0 / 3.0) * (double)p * p * p, 8.0 * (double)p * p);
-        if (p >= 3 && p <= 1024 && need <= max_blocks) {
+        if (p >= 3 && p <= 1024 && need <= max_blocks && !gvec) {
             void *fn;
             int grid_t = need;
             if (env_flag("LYAP_TRIDIAG_REG")) {
@@ -1056,12 +1065,13 @@ int syevd_f64(cudaStream_t s, int p, const double *Ain, double *w_out, double *V
         } else {
             // shared memory for this p (not the capacity): up to two CTAs per SM, one warp
             // per trailing column (the trailing block shrinks: the full grid is best)
-            const size_t smem_p = sizeof(double) * 4 * (size_t)p;
+            const size_t smem_p = smem;
             int dev, nsm, per = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tridiag_kernel, 256, smem_p);
-            const int maxb = nsm * std::max(1, std::min(per, env_flag("LYAP_TRIDIAG_1CTA") ? 1 : 2));
+            int maxb = nsm * std::max(1, std::min(per, env_flag("LYAP_TRIDIAG_1CTA") ? 1 : 2));
+            if (gvec) maxb = std::min(maxb, W.gvec_ctas);
             int grid = std::max(1, std::min(maxb, ceil_div(p - 1, 8)));
             if (const char *e = getenv("LYAP_TRIDIAG_GRID")) grid = std::max(1, std::min(maxb, atoi(e)));
             LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)tridiag_kernel, dim3(grid), dim3(256), args, smem_p, s));

@@ -160,6 +160,57 @@ def test_rank_trunc_chol_parity_sizes(gpu, orc, n, c, r):
     assert np.allclose(Zg, Zo, atol=1e-10 * np.abs(Zo).max())
 
 
+@pytest.mark.parametrize("n,c,r", [(700, 300, 25), (3000, 700, 120), (1500, 1300, 90), (2000, 64, 40)])
+def test_rank_trunc_chol_blocked_parity(gpu, orc, n, c, r, monkeypatch):
+    """Blocked QRCP (xLAQPS scheme: blocks of 32 pivots, read-only GEMV per step, DMMA
+    trailing update per block, early block end on norm cancellation) against the oracle's
+    unblocked RRQR: same rank, same factor."""
+    monkeypatch.setenv("LYAP_RRQR_BLOCKED", "1")
+    rng = np.random.default_rng(n + 3 * c)
+    sv = np.logspace(0, -7, r)
+    Z = (rng.standard_normal((n, r)) * sv[None, :]) @ rng.standard_normal((r, c)) + 1e-12 * rng.standard_normal((n, c))
+    tol = np.sqrt(orc.unit_roundoff("fp32"))
+    Zg = gpu.rank_trunc_chol(colmajor(Z), tol, "fp64").cpu().numpy()
+    Zo = orc.rank_trunc_chol("fp64", Z, tol)
+    assert Zg.shape == Zo.shape
+    assert np.allclose(Zg, Zo, atol=1e-10 * np.abs(Zo).max())
+
+
+@pytest.mark.slow
+def test_rank_trunc_chol_blocked_large(gpu, monkeypatch):
+    """configs[3]-size truncation (n = 16384, c = 3000, blocked path by default): the kept
+    factor reproduces Z Z^T to the RankTruncChol bound (l.1256-1266, reading R-RRQR:
+    ||Z Z^T - Zk Zk^T||_2 <= 2 ||S|| ||Z|| + ||S||^2 with ||S|| <= sqrt(u) |r11|), and the
+    blocked and unblocked paths keep the same rank."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    n, c, r = 16384, 3000, 700
+    sv = torch.logspace(0, -6, r, dtype=torch.float64, device="cuda")
+    Zt = ((torch.randn(n, r, dtype=torch.float64, device="cuda", generator=g) * sv) @
+          torch.randn(r, c, dtype=torch.float64, device="cuda", generator=g)).T.contiguous()
+    tol = 2.0 ** -12
+    Zb = gpu.rank_trunc_chol(Zt, tol, "fp64")
+    monkeypatch.setenv("LYAP_RRQR_BLOCKED", "0")
+    Zu = gpu.rank_trunc_chol(Zt, tol, "fp64")
+    assert Zb.shape == Zu.shape
+    Z = Zt.T
+
+    def norm2(apply, dim, its=60):
+        """2-norm of a symmetric operator by power iteration (converged to a few digits)."""
+        x = torch.randn(dim, dtype=torch.float64, device="cuda", generator=g)
+        lam = 0.0
+        for _ in range(its):
+            y = apply(x)
+            lam = torch.linalg.norm(y).item()
+            x = y / lam
+        return lam
+
+    nZ2 = norm2(lambda x: Z.T @ (Z @ x), c)                       # ||Z||_2^2
+    nD = norm2(lambda x: Z @ (Z.T @ x) - Zb @ (Zb.T @ x), n)       # ||Z Z^T - Zk Zk^T||_2
+    # ||S||_F <= tol |r11| <= tol ||Z||_2
+    assert nD <= (2 * tol + tol ** 2) * nZ2 * 1.05
+    assert torch.linalg.norm(Zb - Zu) <= 1e-9 * torch.linalg.norm(Zu)
+
+
 def test_rank_trunc_chol_parity(gpu, orc):
     rng = np.random.default_rng(3)
     n, c = 200, 40
@@ -198,6 +249,36 @@ def test_newton_aseq_counts(gpu, orc, us, n):
     assert out["steps"] == q.steps
     rt = 1e-12 if us == "fp64" else 50 * orc.unit_roundoff(us)
     assert np.allclose(out["mu"], q.mu, rtol=rt)
+
+
+@pytest.mark.parametrize("us", ["fp64", "fp32", "fp16", "bf16"])
+@pytest.mark.parametrize("n", [100, 128])
+def test_newton_determinantal_scaling(gpu, orc, us, n):
+    """Determinantal scaling mu_k = |det A_k|^{-1/n} (l.1139; log|det| from the Gauss-Jordan
+    pivots): step count and mu_k against the oracle (tc model)."""
+    p = P.paper_synthetic(n, 3, 1.5, seed=1)
+    s = gpu.Solver(n, us=us, max_cols=64, scaling=2)
+    out = s.newton_aseq(cuda(p.A))
+    with orc.model("tc"):
+        q = orc.aseq(us, p.A, scaling="det")
+    assert out["steps"] == q.steps
+    rt = 1e-12 if us == "fp64" else 50 * orc.unit_roundoff(us)
+    assert np.allclose(out["mu"], q.mu, rtol=rt)
+    assert out["inf"][-1] <= 10 * np.sqrt(n * orc.unit_roundoff(us))
+
+
+def test_ir_determinantal_scaling_converges(gpu, orc):
+    """A full IR solve with the determinantal scaling (configs[0], fp16 solver) reaches the
+    fp64 solution and agrees with the oracle run with the same scaling."""
+    p = P.cfg0()
+    s = gpu.Solver(p.n, us="fp16", max_cols=128, scaling=2)
+    res = s.solve(cuda(p.A), colmajor(p.L), None, tol=1e-14, maxit=10)
+    with orc.model("tc"):
+        ro = orc.ir_chol(p.A, p.L, us="fp16", tol=1e-14, imax=10, scaling="det")
+    assert res.report["status"] == ro.status == "converged"
+    assert res.report["steps"] == ro.steps
+    Xg, Xo = _X(res.Z, None), _X(ro.Z, None)
+    assert np.linalg.norm(Xg - Xo) <= 1e-10 * np.linalg.norm(Xo)
 
 
 @pytest.mark.parametrize("ldlt", [False, True])
@@ -349,3 +430,32 @@ def test_ir_capacity_stop_returns_last_iterate(gpu, orc):
         Xg = _X(res.Z, res.Y)
         r_exp = orc.rel_residual_explicit(p.A, Xg, p.W())
         assert np.isfinite(r_exp) and r_exp <= 10 * rep["res"][0]
+
+
+def test_solver_precision_per_solve(gpu):
+    """u_s is an argument of lyap_ir_solve (the paper's problem statement): one handle
+    solving with fp16, then bf16, then fp32, then fp16 again reproduces, bit for bit, the
+    solves of handles created for each precision."""
+    p = P.cfg0()
+    A, L = cuda(p.A), colmajor(p.L)
+    s = gpu.Solver(p.n, us="fp16", max_cols=128)
+    for us in ("fp16", "bf16", "fp32", "fp16"):
+        r = s.solve(A, L, None, tol=1e-14, maxit=10, us=us)
+        ref = gpu.Solver(p.n, us=us, max_cols=128).solve(A, L, None, tol=1e-14, maxit=10)
+        assert r.report["steps"] == ref.report["steps"]
+        assert torch.equal(r.Z, ref.Z), us
+
+
+def test_solve_argument_validation(gpu):
+    """Mistyped or mis-shaped arguments raise before reaching the C ABI."""
+    p = P.cfg0()
+    s = gpu.Solver(p.n, us="fp16", max_cols=128)
+    A, L = cuda(p.A), colmajor(p.L)
+    with pytest.raises(gpu.LyapError):
+        s.solve(A.float(), L)
+    with pytest.raises(gpu.LyapError):
+        s.solve(A[:-1], L)
+    with pytest.raises(gpu.LyapError):
+        s.solve(A, L[:, :-1].contiguous())
+    with pytest.raises(gpu.LyapError):
+        s.solve(A, L, cuda(np.eye(3)))

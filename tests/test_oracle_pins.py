@@ -463,3 +463,35 @@ def test_generators():
     a = P.cfg1(seed=3, n=32).A
     b = P.cfg1(seed=3, n=32).A
     assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- determinantal scaling
+def test_logdet_triangular_closed_form(orc):
+    """log|det| from the LU pivots equals sum log|d_i| for a triangular matrix (|det| is
+    invariant under the row interchanges) and numpy's slogdet for a general one."""
+    rng = np.random.default_rng(21)
+    d = rng.uniform(0.5, 3.0, 12) * np.sign(rng.standard_normal(12))
+    T = np.triu(rng.standard_normal((12, 12)), 1) * 0.1 + np.diag(d)
+    _, _, info, ld = orc.inverse_logdet("fp64", T.T)
+    assert info == 0
+    assert np.isclose(ld, np.sum(np.log(np.abs(d))), rtol=0, atol=1e-13)
+    G = rng.standard_normal((30, 30))
+    _, _, _, ld2 = orc.inverse_logdet("fp64", G)
+    assert np.isclose(ld2, np.linalg.slogdet(G)[1], rtol=1e-13)
+
+
+def test_determinantal_scaling_closed_forms(orc):
+    """mu_0 = |det A|^{-1/n}: for A = -c I, mu_0 = 1/c and A_1 = -I
+    exactly (one Newton step lands on the sign); for a triangular A, the product of the
+    diagonal.  The scaled iteration still converges to -I on a nonnormal stable matrix."""
+    q = orc.aseq("fp64", -4.0 * np.eye(8), scaling="det")
+    assert np.isclose(q.mu[0], 0.25, rtol=1e-15)
+    assert q.inf[0] <= 1e-15                              # ||A_1 + I||_inf = 0
+    rng = np.random.default_rng(22)
+    d = -rng.uniform(0.5, 4.0, 10)
+    T = np.tril(rng.standard_normal((10, 10)), -1) * 0.2 + np.diag(d)
+    q = orc.aseq("fp64", T, scaling="det")
+    assert np.isclose(q.mu[0], np.exp(-np.mean(np.log(np.abs(d)))), rtol=1e-13)
+    p = P.random_stable(25, 2, 3)
+    q = orc.aseq("fp64", p.A, scaling="det")
+    assert q.converged and q.inf[-1] <= 10 * np.sqrt(25 * 2.0 ** -53)

@@ -13,7 +13,8 @@ classes = sys.argv[4].split(",") if len(sys.argv) > 4 else list(G.KERNEL_CLASSES
 A = torch.tensor(p.A, dtype=torch.float64, device="cuda")
 Lt = torch.tensor(np.ascontiguousarray(p.L.T), dtype=torch.float64, device="cuda")
 S = torch.tensor(p.S, dtype=torch.float64, device="cuda") if p.S is not None else None
-s = G.Solver(p.n, us=us, max_cols=mc)
+s = G.Solver(p.n, us=us, max_cols=mc, newton_cols=int(os.environ.get("NEWTON_COLS", "0")),
+             work_cols=int(os.environ.get("WORK_COLS", "0")))
 t = time.time(); r = s.solve(A, Lt, S, tol=1e-14, maxit=30); torch.cuda.synchronize()
 print(f"{cfg} {us} solve wall %.3f s" % (time.time() - t), json.dumps({k: v for k, v in r.report.items()}), flush=True)
 for name in classes:
