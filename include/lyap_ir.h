@@ -58,7 +58,7 @@ typedef struct {
                            paper's choice, l.1406; default), 2 determinantal
                            scaling |det A_k|^{-1/n} from the inversion's pivots */
     int    extra;       /* Newton iterations after Eq. newton-stop-tau holds
-                           (reading R-EXTRA: 1, matches Table 4) */
+                           (reading R-EXTRA: 1, matches Table 3, l.1449) */
     double rho;         /* rank truncation threshold rho (l.1424: 0.1) */
     double eta_r;       /* residual truncation, relative (l.1428: 1e-4) */
     double eta_s;       /* solution truncation, relative (l.1427: 10u) */

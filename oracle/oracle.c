@@ -370,7 +370,7 @@ int orc_syev(int p, int n, const double *A, double *w, double *V)
 /* side computations; as in the paper's chop-based simulation (only the   */
 /* n x n work emulated, l.1400-1401) they run in binary64 and their       */
 /* outputs are rounded to the solver precision.  Evidence: with this      */
-/* reading the LDL^T bf16 column of Table 4 (n=100) is reproduced         */
+/* reading the LDL^T bf16 column of Table 3 (n=100, l.1449-1506) is reproduced         */
 /* (12(2) at cond 1.3 vs the paper's 12(2)); with emulated internals it   */
 /* is 42(2).                                                              */
 /* RankTruncChol (l.1256-1266): rank-revealing QR Z^T Pi = Q [T C; 0 S]  */

@@ -774,7 +774,7 @@ int GjeWork::alloc(int n_, int prec_) {
     LYAP_CUDA_TRY(cudaMalloc(&tmp, es * (size_t)n * 2 * b));
     LYAP_CUDA_TRY(cudaMalloc(&Pglob, acc * (size_t)n * b));
     LYAP_CUDA_TRY(cudaMalloc(&Tg, acc * 2 * 32 * 32));   // T, then Linv
-    if ((prec == LYAP_FP16 || prec == LYAP_BF16) && n % 8 == 0 && n >= 2 * GJE_NB) {
+    if ((prec == LYAP_FP16 || prec == LYAP_BF16 || prec == LYAP_FP32) && n % 8 == 0 && n >= 2 * GJE_NB) {
         LYAP_CUDA_TRY(cudaMalloc(&Bo, es * (size_t)n * GJE_NB));
         LYAP_CUDA_TRY(cudaMalloc(&tmp2, es * (size_t)n * 2 * GJE_NB));
         LYAP_CUDA_TRY(cudaMalloc(&oints, sizeof(int) * (5 * GJE_NB + 8 + (size_t)n)));
@@ -936,6 +936,18 @@ static int gje_panel_launch(cudaStream_t s, int n, int k, int b, T *A, GjeWork &
     return launched();
 }
 
+// C (M x N, row-major, ld ldc) += A (M x K, row-major) B^T (B: N x K row-major) for the
+// two-level sweep: tcgen05 for the 16-bit types, the 128 x 128 SIMT kernel for fp32.
+template <typename T>
+static int outer_gemm(cudaStream_t s, int M, int N, int K, const T *A, long lda, const T *B, long ldb, T *C,
+                      long ldc, int cap = 0)
+{
+    if constexpr (std::is_same<T, float>::value)
+        return gemm_strided<float, float, float, float>(s, M, N, K, 1.0f, A, lda, 1, B, 1, ldb, 1.0f, C, ldc, 1);
+    else
+        return tc_gemm(s, Prec<T>::code, M, N, K, 1.0f, A, lda, B, ldb, 1.0f, C, ldc, 0, cap);
+}
+
 template <typename T>
 static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
 {
@@ -945,11 +957,12 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
     LYAP_CUDA_TRY(cudaMemsetAsync(w.ldet, 0, sizeof(double) * (size_t)n, s));
     iota_kernel<<<ceil_div(n, 256), 256, 0, s>>>(n, w.rowperm);
     LYAP_TRY(launched());
-    // two-level blocking for the 16-bit types: inner 32-wide steps restricted to an
-    // outer block of NB columns, then one rank-NB tensor-core update of the rest
+    // two-level blocking for the 16-bit types and fp32: inner 32-wide steps restricted to an
+    // outer block of NB columns, then one rank-NB update of the rest (tcgen05 / SIMT fp32)
     constexpr bool half_t = std::is_same<T, __half>::value || std::is_same<T, __nv_bfloat16>::value;
-    const bool two_level = half_t && !use_simt_gemm() && n % 8 == 0 && n >= 2 * GJE_NB && w.Bo != nullptr &&
-                           !env_flag("LYAP_GJE_1LEVEL");
+    constexpr bool f32_t = std::is_same<T, float>::value;
+    const bool two_level = (half_t || f32_t) && !(half_t && use_simt_gemm()) && n % 8 == 0 && n >= 2 * GJE_NB &&
+                           w.Bo != nullptr && !env_flag("LYAP_GJE_1LEVEL");
     const int NBo = two_level ? GJE_NB : n;
     // look-ahead (two-level only): the inner steps (pivot panels) of block K0+NB run on the
     // high-priority side stream P while the main stream finishes the outer update of block
@@ -991,8 +1004,7 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
             {
                 KTimer kt(KC_GJE_UPDATE, P);
                 if (two_level)
-                    LYAP_TRY(tc_gemm(P, Prec<T>::code, n, nbk, b, 1.0f, w.X, b, (const T *)w.B + (size_t)K0 * b, b,
-                                     1.0f, A + K0, n, 0));
+                    LYAP_TRY(outer_gemm<T>(P, n, nbk, b, (const T *)w.X, b, (const T *)w.B + (size_t)K0 * b, b, A + K0, n));
                 else
                     LYAP_TRY(gemm_update(P, n, b, (const T *)w.X, (const T *)w.B, A));
             }
@@ -1025,19 +1037,17 @@ static int gje_invert_t(cudaStream_t s, int n, T *A, GjeWork &w)
             const int cr = K0 + nbk;
             const int cn = ahead ? std::min(n, cr + NBo) : cr;
             if (ahead && cn > cr) {
-                LYAP_TRY(tc_gemm(s, Prec<T>::code, n, cn - cr, nbk, 1.0f, A + K0, n, (const T *)w.Bo + (size_t)cr * nbk,
-                                 nbk, 1.0f, A + cr, n, 0));
+                LYAP_TRY(outer_gemm<T>(s, n, cn - cr, nbk, A + K0, n, (const T *)w.Bo + (size_t)cr * nbk, nbk, A + cr, n));
                 LYAP_CUDA_TRY(cudaEventRecord(w.ev_a, s));
                 LYAP_CUDA_TRY(cudaStreamWaitEvent(P, w.ev_a, 0));
             }
             // with look-ahead, leave SMs for the pivot-panel cluster running concurrently on P
             const int cap = ahead ? 148 - 16 : 0;
             if (K0 > 0)
-                LYAP_TRY(tc_gemm(s, Prec<T>::code, n, K0, nbk, 1.0f, A + K0, n, (const T *)w.Bo, nbk, 1.0f, A, n, 0,
-                                 cap));
+                LYAP_TRY(outer_gemm<T>(s, n, K0, nbk, A + K0, n, (const T *)w.Bo, nbk, A, n, cap));
             if (cn < n)
-                LYAP_TRY(tc_gemm(s, Prec<T>::code, n, n - cn, nbk, 1.0f, A + K0, n, (const T *)w.Bo + (size_t)cn * nbk,
-                                 nbk, 1.0f, A + cn, n, 0, cap));
+                LYAP_TRY(outer_gemm<T>(s, n, n - cn, nbk, A + K0, n, (const T *)w.Bo + (size_t)cn * nbk, nbk, A + cn, n,
+                                       cap));
         }
     }
     invperm_kernel<<<ceil_div(n, 256), 256, 0, s>>>(n, w.rowperm, w.invperm);

@@ -34,7 +34,9 @@ struct lyap_ir_ctx {
     size_t es = 0;
     // A side
     void *Ak = nullptr, *An = nullptr, *W = nullptr;
-    std::vector<void *> inv;
+    std::vector<void *> inv;   // cached Gauss-Jordan results G_k (u_s, column-permuted, 2^e-scaled)
+    std::vector<int *> perms;  // per cached step: rowperm (n) and invperm (n) of the inversion
+    std::vector<int> iexp;     // per cached step: range-scaling exponent e_k
     int ksteps = 0;
     std::vector<double> mu, delta, infn;
     GjeWork gje;
@@ -92,25 +94,32 @@ int sync_read(lyap_ir_ctx *h, void *dst, const void *src, size_t bytes) {
     return LYAP_OK;
 }
 
-// C (n x c, col-major) = Ainv (n x n row-major, u_s) * Z (n x c, col-major, u_s)
-int zside_gemm(lyap_ir_ctx *h, const void *Ainv, const void *Z, void *Out, int c) {
+// C (n x c, col-major) = A_j^{-1} Z (Z n x c, col-major, u_s).  The cache holds the
+// Gauss-Jordan result G_j as computed (A_j^{-1}[i][l] = 2^{-e_j} G_j[i][invperm_j[l]]), so
+// A_j^{-1} Z = 2^{-e_j} G_j Z' with Z'[t] = Z[rowperm_j[t]]: one row gather of Z (n c
+// elements) replaces an n^2 un-permuted copy of the inverse in the Newton update.
+int zside_gemm(lyap_ir_ctx *h, int j, const void *Z, void *Out, int c) {
     const int n = h->n;
+    const void *G = h->inv[j];
+    LYAP_TRY(nk_row_gather(h->s, h->us, n, c, Z, h->perms[j], h->W));
+    const void *Zp = h->W;
+    const double alpha = std::ldexp(1.0, -h->iexp[j]);
     if ((h->us == LYAP_BF16 || h->us == LYAP_FP16) && !use_simt_gemm() && n % 8 == 0)
-        // Out (n x c, column-major) = Ainv (n x n, row-major = K-major) * Z, Z^T rows K-major
-        return tc_gemm(h->s, h->us, n, c, n, 1.0f, Ainv, n, Z, n, 0.0f, Out, n, 1);
+        // Out (n x c, column-major) = G (n x n, row-major = K-major) * Z', Z'^T rows K-major
+        return tc_gemm(h->s, h->us, n, c, n, (float)alpha, G, n, Zp, n, 0.0f, Out, n, 1);
     switch (h->us) {
         case LYAP_FP64:
-            return gemm_strided<double, double, double, double>(h->s, n, c, n, 1.0, (const double *)Ainv, n, 1,
-                                                                (const double *)Z, 1, n, 0.0, (double *)Out, 1, n);
+            return gemm_strided<double, double, double, double>(h->s, n, c, n, alpha, (const double *)G, n, 1,
+                                                                (const double *)Zp, 1, n, 0.0, (double *)Out, 1, n);
         case LYAP_FP32:
-            return gemm_strided<float, float, float, float>(h->s, n, c, n, 1.0f, (const float *)Ainv, n, 1,
-                                                            (const float *)Z, 1, n, 0.0f, (float *)Out, 1, n);
+            return gemm_strided<float, float, float, float>(h->s, n, c, n, (float)alpha, (const float *)G, n, 1,
+                                                            (const float *)Zp, 1, n, 0.0f, (float *)Out, 1, n);
         case LYAP_FP16:
-            return gemm_strided<__half, __half, __half, float>(h->s, n, c, n, 1.0f, (const __half *)Ainv, n, 1,
-                                                               (const __half *)Z, 1, n, 0.0f, (__half *)Out, 1, n);
+            return gemm_strided<__half, __half, __half, float>(h->s, n, c, n, (float)alpha, (const __half *)G, n, 1,
+                                                               (const __half *)Zp, 1, n, 0.0f, (__half *)Out, 1, n);
         case LYAP_BF16:
             return gemm_strided<__nv_bfloat16, __nv_bfloat16, __nv_bfloat16, float>(
-                h->s, n, c, n, 1.0f, (const __nv_bfloat16 *)Ainv, n, 1, (const __nv_bfloat16 *)Z, 1, n, 0.0f,
+                h->s, n, c, n, (float)alpha, (const __nv_bfloat16 *)G, n, 1, (const __nv_bfloat16 *)Zp, 1, n, 0.0f,
                 (__nv_bfloat16 *)Out, 1, n);
     }
     return LYAP_ERR_ARG;
@@ -133,20 +142,32 @@ int aseq_compute(lyap_ir_ctx *h, const double *A) {
             void *p = nullptr;
             LYAP_TRY(dmalloc(&p, h->es * nn));
             h->inv.push_back(p);
+            int *pp = nullptr;
+            LYAP_TRY(dalloc(&pp, 2 * (size_t)n));
+            h->perms.push_back(pp);
         }
-        LYAP_TRY(nk_scale(s, us, nn, h->Ak, h->W, h->scal));
-        LYAP_TRY(gje_invert(s, n, us, h->W, h->gje));
+        if ((int)h->iexp.size() < it) h->iexp.push_back(0);
+        // W = 2^{-e} A_k goes straight into the cache slot and is inverted in place there
+        // (the Newton update then streams A_k and G in and A_{k+1} out: three n^2 streams)
+        void *G = h->inv[it - 1];
+        LYAP_TRY(nk_scale(s, us, nn, h->Ak, G, h->scal));
+        LYAP_TRY(gje_invert(s, n, us, G, h->gje));
         // mu_k: Frobenius-norm scaling (opt.scaling = 1, the paper's choice l.1406) or
         // determinantal scaling |det A_k|^{-1/n} (opt.scaling = 2, l.1139)
         if (h->opt.scaling == 2) LYAP_TRY(nk_mu_det(s, n, h->gje.ldet, h->scal, scaling_on));
-        else LYAP_TRY(nk_mu(s, us, n, h->W, h->part, h->scal, scaling_on));
-        LYAP_TRY(nk_update(s, us, n, h->Ak, h->W, h->gje.invperm, h->An, h->inv[it - 1], h->scal, h->part));
+        else LYAP_TRY(nk_mu(s, us, n, G, h->part, h->scal, scaling_on));
+        LYAP_TRY(nk_update(s, us, n, h->Ak, G, h->gje.invperm, h->An, nullptr, h->scal, h->part));
+        LYAP_CUDA_TRY(cudaMemcpyAsync(h->perms[it - 1], h->gje.rowperm, sizeof(int) * (size_t)n,
+                                      cudaMemcpyDeviceToDevice, s));
+        LYAP_CUDA_TRY(cudaMemcpyAsync(h->perms[it - 1] + n, h->gje.invperm, sizeof(int) * (size_t)n,
+                                      cudaMemcpyDeviceToDevice, s));
         LYAP_TRY(nk_roll(s, h->scal));
         int info = 0;
         LYAP_CUDA_TRY(cudaMemcpyAsync(&info, h->gje.info, sizeof(int), cudaMemcpyDeviceToHost, s));
         LYAP_TRY(sync_read(h, h->hscal, h->scal, sizeof(double) * SC_COUNT));
         if (info != 0) return LYAP_ERR_SINGULAR;
         const double *sc = h->hscal;
+        h->iexp[it - 1] = (int)sc[SC_EXP];
         double delta = std::sqrt(sc[SC_RED + 0]) / std::sqrt(sc[SC_RED + 1]);
         double inf = sc[SC_RED + 2];
         if (!std::isfinite(sc[SC_RED + 3]) || !std::isfinite(delta)) return LYAP_ERR_OVERFLOW;
@@ -240,7 +261,7 @@ int zside(lyap_ir_ctx *h, bool ldlt, const double *L, int m, const double *S, do
         const double mu = h->mu[j];
         {
             KTimer kt(KC_ZSIDE_GEMM, s);
-            LYAP_TRY(zside_gemm(h, h->inv[j], h->Zt, (void *)(Zbytes + h->es * (size_t)n * c), c));
+            LYAP_TRY(zside_gemm(h, j, h->Zt, (void *)(Zbytes + h->es * (size_t)n * c), c));
         }
         if (ldlt) {
             LYAP_TRY(nk_y_blkdiag(s, c, h->Yc, h->PZ, h->Yn, h->PZ, mu / 2.0, 1.0 / (2.0 * mu), us));
@@ -448,7 +469,10 @@ int set_precision(lyap_ir_ctx *h, int us) {
     LYAP_CUDA_TRY(cudaStreamSynchronize(h->s));
     for (void *p : {h->Ak, h->An, h->W, h->Zt}) cudaFree(p);
     for (void *p : h->inv) cudaFree(p);
+    for (int *p : h->perms) cudaFree(p);
     h->inv.clear();
+    h->perms.clear();
+    h->iexp.clear();
     h->ksteps = 0;
     h->Ak = h->An = h->W = h->Zt = nullptr;
     h->gje.release();
@@ -458,7 +482,7 @@ int set_precision(lyap_ir_ctx *h, int us) {
     const size_t nn = (size_t)h->n * h->n;
     LYAP_TRY(dmalloc(&h->Ak, h->es * nn));
     LYAP_TRY(dmalloc(&h->An, h->es * nn));
-    LYAP_TRY(dmalloc(&h->W, h->es * nn));
+    LYAP_TRY(dmalloc(&h->W, h->es * (size_t)h->n * h->PZ));
     LYAP_TRY(dmalloc(&h->Zt, h->es * (size_t)h->n * h->PZ));
     return h->gje.alloc(h->n, us);
 }
@@ -639,7 +663,7 @@ int lyap_ir_create(lyap_ir_handle *out, int n, int cmax, int us, const lyap_ir_o
     auto A = [&](int r) { if (rc == LYAP_OK) rc = r; };
     A(dmalloc(&h->Ak, h->es * nn));
     A(dmalloc(&h->An, h->es * nn));
-    A(dmalloc(&h->W, h->es * nn));
+    A(dmalloc(&h->W, h->es * (size_t)n * h->PZ));      // row-gathered Z' of the Z-side product
     A(h->gje.alloc(n, us));
     A(h->qr.alloc(n, h->PW));
     A(h->eig.alloc(std::min(n, h->PW)));
@@ -679,6 +703,7 @@ int lyap_ir_destroy(lyap_ir_handle h) {
     cudaStreamSynchronize(h->s);
     for (void *p : {h->Ak, h->An, h->W, h->Zt}) cudaFree(p);
     for (void *p : h->inv) cudaFree(p);
+    for (int *p : h->perms) cudaFree(p);
     h->gje.release(); h->qr.release(); h->eig.release(); h->rrqr.release();
     for (void *p : {(void *)h->scal, (void *)h->part, (void *)h->ibuf, (void *)h->Yc, (void *)h->Yn, (void *)h->Zd,
                     (void *)h->Zd2, (void *)h->F, (void *)h->U, (void *)h->Tm, (void *)h->Nm, (void *)h->TN,
@@ -738,7 +763,9 @@ int lyap_newton_aseq(lyap_ir_handle h, const double *A, int *steps, double *mu, 
 
 int lyap_newton_get_inverse(lyap_ir_handle h, int j, void *out) {
     if (!h || !out || j < 0 || j >= h->ksteps) return LYAP_ERR_ARG;
-    LYAP_CUDA_TRY(cudaMemcpyAsync(out, h->inv[j], h->es * (size_t)h->n * h->n, cudaMemcpyDeviceToDevice, h->s));
+    // A_j^{-1}[i][l] = 2^{-e_j} G_j[i][invperm_j[l]]
+    LYAP_TRY(col_gather(h->s, h->n, h->us, h->inv[j], h->perms[j] + h->n, out));
+    LYAP_TRY(nk_ldexp(h->s, h->us, (long)h->n * h->n, out, -h->iexp[j]));
     LYAP_CUDA_TRY(cudaStreamSynchronize(h->s));
     return LYAP_OK;
 }

@@ -213,7 +213,7 @@ newton_update_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ G, c
             T gi;
             if constexpr (sizeof(T) == 8) gi = ldexp(G[(long)i * n + invperm[j]], -e);
             else gi = from_f<T>(ldexpf(to_f<T>(G[(long)i * n + invperm[j]]), -e));
-            Ainv[(long)i * n + j] = gi;
+            if (Ainv) Ainv[(long)i * n + j] = gi;
             Acc x = to_acc<T>(Ak[(long)i * n + j]);
             Acc y = to_acc<T>(gi);
             T nv = from_acc<T>(Acc(0.5) * fma(a, x, b * y));
@@ -263,7 +263,7 @@ newton_update_row_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ 
         __syncthreads();
         const uint4 *Ai = reinterpret_cast<const uint4 *>(Ak + (long)i * n);
         uint4 *Ni = reinterpret_cast<uint4 *>(Anext + (long)i * n);
-        uint4 *Ii = reinterpret_cast<uint4 *>(Ainv + (long)i * n);
+        uint4 *Ii = Ainv ? reinterpret_cast<uint4 *>(Ainv + (long)i * n) : nullptr;
         double dd = 0.0, ss = 0.0, rs = 0.0, mx = 0.0;
         for (int jv = threadIdx.x; jv < nv; jv += blockDim.x) {
             uint4 av = __ldcs(Ai + jv), iv, nw;
@@ -287,7 +287,7 @@ newton_update_row_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ 
                 mx = fmax(mx, fabs(nd));
                 if (!isfinite(nd)) mx = INFINITY;
             }
-            Ii[jv] = iv;
+            if (Ii) Ii[jv] = iv;
             Ni[jv] = nw;
         }
         dd = block_sum(dd, red); ss = block_sum(ss, red);     // block_sum's barriers also
@@ -593,6 +593,49 @@ int nk_mu(cudaStream_t s, int prec, int n, const void *G, double *part, double *
     return launched();
 }
 
+// Z' (n x c, column-major) = rows of Z in the Gauss-Jordan pivot order: Z'[t] = Z[rowperm[t]],
+// so that A_k^{-1} Z = 2^{-e} G Z' with the cached, column-permuted G (Section 3.4 cache).
+template <typename T>
+__global__ void row_gather_kernel(int n, long len, const T *__restrict__ Z, const int *__restrict__ rowperm,
+                                  T *__restrict__ out)
+{
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < len; idx += (long)gridDim.x * blockDim.x) {
+        const long col = idx / n;
+        const int t = (int)(idx - col * n);
+        out[idx] = Z[col * n + rowperm[t]];
+    }
+}
+template <typename T> static void k_row_gather(cudaStream_t s, int n, int c, const void *Z, const int *rp, void *out)
+{
+    const long len = (long)n * c;
+    row_gather_kernel<T><<<grid_for(len), 256, 0, s>>>(n, len, (const T *)Z, rp, (T *)out);
+}
+int nk_row_gather(cudaStream_t s, int prec, int n, int c, const void *Z, const int *rowperm, void *out)
+{
+    if ((long)n * c <= 0) return LYAP_OK;
+    DISPATCH_T(prec, k_row_gather, s, n, c, Z, rowperm, out);
+    return launched();
+}
+
+// x <- 2^e x (exact power-of-two scaling in the element type)
+template <typename T>
+__global__ void ldexp_kernel(long len, T *__restrict__ x, int e)
+{
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < len; i += (long)gridDim.x * blockDim.x) {
+        if constexpr (sizeof(T) == 8) x[i] = ldexp(x[i], e);
+        else x[i] = from_f<T>(ldexpf(to_f<T>(x[i]), e));
+    }
+}
+template <typename T> static void k_ldexp(cudaStream_t s, long len, void *x, int e)
+{
+    ldexp_kernel<T><<<grid_for(len), 256, 0, s>>>(len, (T *)x, e);
+}
+int nk_ldexp(cudaStream_t s, int prec, long len, void *x, int e)
+{
+    DISPATCH_T(prec, k_ldexp, s, len, x, e);
+    return launched();
+}
+
 int nk_mu_det(cudaStream_t s, int n, const double *ldet, double *scal, int scaling)
 {
     mu_det_kernel<<<1, 256, 0, s>>>(n, scaling, ldet, scal);
@@ -629,7 +672,8 @@ int nk_update(cudaStream_t s, int prec, int n, const void *Ak, const void *G, co
 {
     {
         const double es = prec == LYAP_FP64 ? 8.0 : prec == LYAP_FP32 ? 4.0 : 2.0;
-        KTimer kt(KC_NEWTON_UPDATE, s, 0.0, 4.0 * es * (double)n * n);
+        // algorithmic bytes: A_k and G in, A_{k+1} out (+ the cached A_k^{-1} if requested)
+        KTimer kt(KC_NEWTON_UPDATE, s, 0.0, (Ainv ? 4.0 : 3.0) * es * (double)n * n);
         DISPATCH_T(prec, k_update, s, n, Ak, G, invperm, Anext, Ainv, scal, part);
     }
     LYAP_TRY(launched());

@@ -25,6 +25,8 @@ int nk_cast(cudaStream_t s, int prec, int n, const double *A, void *Ak, double *
 int nk_scale(cudaStream_t s, int prec, long nn, const void *Ak, void *W, double *scal);
 int nk_mu(cudaStream_t s, int prec, int n, const void *G, double *part, double *scal, int scaling);
 int nk_mu_det(cudaStream_t s, int n, const double *ldet, double *scal, int scaling);
+int nk_row_gather(cudaStream_t s, int prec, int n, int c, const void *Z, const int *rowperm, void *out);
+int nk_ldexp(cudaStream_t s, int prec, long len, void *x, int e);
 int nk_update(cudaStream_t s, int prec, int n, const void *Ak, const void *G, const int *invperm, void *Anext,
               void *Ainv, double *scal, double *part);
 int nk_roll(cudaStream_t s, double *scal);

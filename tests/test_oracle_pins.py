@@ -370,7 +370,7 @@ def test_ir_fp64_equals_kron(orc, seed):
 
 @pytest.mark.parametrize("us", ["fp32", "fp16", "bf16"])
 def test_ir_low_precision_solver_reaches_fp64(orc, us):
-    """Table 3 / Theorems 2.1-2.2: u_s in {fp32, fp16, bf16}, u_r = u_c = fp64 gives an
+    """Table 2 (l.1078) / Theorems 2.1-2.2: u_s in {fp32, fp16, bf16}, u_r = u_c = fp64 gives an
     fp64-level residual for kappa well below 1/u_s."""
     p = P.random_stable(10, 2, 21)
     W = p.W()
@@ -386,12 +386,12 @@ def test_ir_low_precision_solver_reaches_fp64(orc, us):
         assert all(b < a for a, b in zip(r.res, r.res[1:]))
 
 
-def test_table4_newton_counts(orc):
-    """PAPER.md Table 4 (golden/table4_alpha_n100.txt): the per-call Newton counts alpha
+def test_table3_newton_counts(orc):
+    """PAPER.md Table 3 (l.1449-1506, golden/table3_alpha_n100.txt): the per-call Newton counts alpha
     of the n=100 Cholesky block for u_s in {bf16, fp32, fp64} are reproduced exactly by the
     A-side of Algorithms 3/4 with Frobenius scaling, the delta-rules of Section 4 and one
     extra iteration (reading R-EXTRA)."""
-    for line in open(os.path.join(GOLD, "table4_alpha_n100.txt")):
+    for line in open(os.path.join(GOLD, "table3_alpha_n100.txt")):
         if line.startswith("#") or not line.strip():
             continue
         cond, q, a16, a32, a64 = line.split()
@@ -400,8 +400,8 @@ def test_table4_newton_counts(orc):
         assert got == [int(a16), int(a32), int(a64)], (cond, got)
 
 
-def test_ir_iteration_trend_table4(orc):
-    """Acceptance 4 (Table 4 pattern): total Newton iterations grow and the per-call count
+def test_ir_iteration_trend_table3(orc):
+    """Acceptance 4 (Table 3 pattern, l.1449-1506): total Newton iterations grow and the per-call count
     shrinks as u_s is lowered (paper_synthetic n=100, q=0.5)."""
     p = P.paper_synthetic(100, 3, 0.5, seed=0)
     tot, mx = {}, {}

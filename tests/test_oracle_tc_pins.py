@@ -122,7 +122,7 @@ def test_tc_model_is_exact_for_fp32_and_fp64(orc):
 def test_tc_ir_reaches_model_independent_solution(orc, us):
     """The tc-model IR on configs[0] (reduced n) converges to the fp64 Kronecker solution
     (Eq. lyap-ls, a model-independent reference) -- the model changes the path, not
-    the limit (Table 3 semantics, l.1078)."""
+    the limit (Table 2 semantics, l.1078)."""
     p = P.cfg0(n=24, m=2)
     X = orc.kron_solve(p.A, p.W())
     with orc.model("tc"):
