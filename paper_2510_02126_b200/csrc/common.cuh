@@ -31,12 +31,15 @@ extern std::atomic<int64_t> g_launches;
         if (_r != LYAP_OK) return _r;  \
     } while (0)
 
-// Count a launch and check for launch errors.
-inline int launched() {
+// Count a launch and check for launch errors.  LYAP_SYNC_DEBUG=1 synchronises after every
+// launch and names the launch site of an asynchronous fault (debugging only).
+inline int launched(const char *file = __builtin_FILE(), int line = __builtin_LINE()) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
+    static const bool sync_dbg = [] { const char *v = getenv("LYAP_SYNC_DEBUG"); return v && v[0] == '1'; }();
+    if (e == cudaSuccess && sync_dbg) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
-        fprintf(stderr, "lyap: launch error %s\n", cudaGetErrorString(e));
+        fprintf(stderr, "lyap: launch error %s (launch at %s:%d)\n", cudaGetErrorString(e), file, line);
         return LYAP_ERR_CUDA;
     }
     return LYAP_OK;

@@ -79,7 +79,7 @@ struct RrqrWork {
     double *M = nullptr, *nrm = nullptr, *scal = nullptr;
     int *ints = nullptr;
     // blocked QRCP: reflectors (cmax x 32), F (nmax x 32), partials, state
-    double *V3 = nullptr, *F3 = nullptr, *p3 = nullptr, *st3 = nullptr;
+    double *V3 = nullptr, *F3 = nullptr, *p3 = nullptr, *st3 = nullptr, *ug3 = nullptr, *pw3 = nullptr;
     int *act3 = nullptr, *ist3 = nullptr;
     int p3_ctas = 0;
     int alloc(int nmax, int cmax);

@@ -265,27 +265,47 @@ newton_update_row_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ 
         uint4 *Ni = reinterpret_cast<uint4 *>(Anext + (long)i * n);
         uint4 *Ii = Ainv ? reinterpret_cast<uint4 *>(Ainv + (long)i * n) : nullptr;
         double dd = 0.0, ss = 0.0, rs = 0.0, mx = 0.0;
+        constexpr bool half_t = sizeof(T) == 2;
+        const float scf = ldexpf(1.0f, -e);           // 2^-e: x * 2^-e rounds exactly as ldexp does
+        const double scd = ldexp(1.0, -e);
         for (int jv = threadIdx.x; jv < nv; jv += blockDim.x) {
             uint4 av = __ldcs(Ai + jv), iv, nw;
             const T *ae = reinterpret_cast<const T *>(&av);
             T *ie = reinterpret_cast<T *>(&iv), *ne = reinterpret_cast<T *>(&nw);
+            // 16-bit types: the row partials of the V = 8 elements of this vector in fp32
+            // (squares of 11-bit significands and their differences are exact or rounded once),
+            // then added to the fp64 accumulators -- fp64 work per vector, not per element
+            float ddf = 0.f, ssf = 0.f, rsf = 0.f, mxf = 0.f;
 #pragma unroll
             for (int t = 0; t < V; t++) {
                 const int j = jv * V + t;
                 T gi;
-                if constexpr (sizeof(T) == 8) gi = ldexp(g[invperm[j]], -e);
-                else gi = from_f<T>(ldexpf(to_f<T>(g[invperm[j]]), -e));
+                if constexpr (sizeof(T) == 8) gi = g[invperm[j]] * scd;
+                else gi = from_f<T>(to_f<T>(g[invperm[j]]) * scf);
                 ie[t] = gi;
                 Acc x = to_acc<T>(ae[t]);
                 Acc y = to_acc<T>(gi);
                 T nvt = from_acc<T>(Acc(0.5) * fma(a, x, b * y));
                 ne[t] = nvt;
-                double nd = to_d<T>(nvt), xd = (double)x;
-                dd = fma(nd - xd, nd - xd, dd);
-                ss = fma(nd, nd, ss);
-                rs += fabs(nd + (i == j ? 1.0 : 0.0));
-                mx = fmax(mx, fabs(nd));
-                if (!isfinite(nd)) mx = INFINITY;
+                if constexpr (half_t) {
+                    const float nd = to_f<T>(nvt), df = nd - (float)x;
+                    ddf = fmaf(df, df, ddf);
+                    ssf = fmaf(nd, nd, ssf);
+                    rsf += fabsf(nd + (i == j ? 1.0f : 0.0f));
+                    mxf = fmaxf(mxf, fabsf(nd));
+                    if (!isfinite(nd)) mxf = INFINITY;
+                } else {
+                    double nd = to_d<T>(nvt), xd = (double)x;
+                    dd = fma(nd - xd, nd - xd, dd);
+                    ss = fma(nd, nd, ss);
+                    rs += fabs(nd + (i == j ? 1.0 : 0.0));
+                    mx = fmax(mx, fabs(nd));
+                    if (!isfinite(nd)) mx = INFINITY;
+                }
+            }
+            if constexpr (half_t) {
+                dd += (double)ddf; ss += (double)ssf; rs += (double)rsf;
+                mx = fmax(mx, (double)mxf);
             }
             if (Ii) Ii[jv] = iv;
             Ni[jv] = nw;

@@ -388,6 +388,8 @@ struct Rrqr3Args {
     int *active;        // n: 1 while not pivoted
     double *state;      // [0] r11
     int *istate;        // [0] next j, [1] done (rank final), [2] rank
+    double *ug;         // c: the updated pivot column u (row slices by CTA)
+    double *pw;         // gridDim x (RQ_NB + 1): slice partials of V^T u and ||u||^2
 };
 
 __global__ void __launch_bounds__(256, 2)
@@ -475,17 +477,58 @@ rrqr3_kernel(Rrqr3Args a)
         if (s_fl) break;                     // a downdate cancelled in the previous step: end the block
         if ((j > 0 && tr <= a.tol * r11) || tr == 0.0 || bi >= n) { stopped = 1; break; }
         const int pc = bi;
-        // ---- u = M[j0:, pc] - V[j0:, 0:jj] F[pc, 0:jj]^T; reflector from u[j:]
+        // ---- u = M[j:, pc] - V[j:, 0:jj] F[pc, 0:jj]^T, split over the CTAs by row slices
+        // (every CTA forming all of u would read V (c x jj) from L2 G times per step), with
+        // each slice's partial ||u[j+1:]||^2 and V[j+1:, l]^T u[j+1:] (l < jj); one more
+        // grid barrier publishes u and the partials
         const double *xp = a.M + (long)pc * c;
         const double *Fp = a.F + (long)pc * RQ_NB;
-        double part = 0.0;
-        for (int i = j + threadIdx.x; i < c; i += blockDim.x) {
-            double x = xp[i];
-            for (int l = 0; l < jj; l++) x = fma(-a.V[(long)l * c + i], Fp[l], x);
-            ush[i] = x;
-            if (i > j) part = fma(x, x, part);
+        if (wib == 0) {                              // one warp per CTA: <= ~50 rows per slice
+            const int rows = c - j, per = (rows + G - 1) / G;
+            const int r0 = j + blockIdx.x * per, r1 = min(c, r0 + per);
+            double pn = 0.0;
+            double pwl[RQ_NB];
+#pragma unroll
+            for (int l = 0; l < RQ_NB; l++) pwl[l] = 0.0;
+            for (int i = r0 + lane; i < r1; i += 32) {
+                double x = xp[i];
+                for (int l = 0; l < jj; l++) x = fma(-a.V[(long)l * c + i], Fp[l], x);
+                a.ug[i] = x;
+                if (i > j) {
+                    pn = fma(x, x, pn);
+#pragma unroll
+                    for (int l = 0; l < RQ_NB; l++)
+                        if (l < jj) pwl[l] = fma(a.V[(long)l * c + i], x, pwl[l]);
+                }
+            }
+            pn = warp_sum(pn);
+            double *pq = a.pw + (long)blockIdx.x * (RQ_NB + 1);
+            if (lane == 0) pq[RQ_NB] = pn;
+#pragma unroll
+            for (int l = 0; l < RQ_NB; l++) {
+                if (l < jj) {                        // jj is uniform: no divergence
+                    const double t2 = warp_sum(pwl[l]);
+                    if (lane == 0) pq[l] = t2;
+                }
+            }
         }
-        part = block_sum(part, red);
+        grid.sync();
+        double part = 0.0;
+        if (wib == 0) {
+            for (int b = lane; b < G; b += 32) part += __ldcg(a.pw + (long)b * (RQ_NB + 1) + RQ_NB);
+            part = warp_sum(part);
+        }
+        // warps 1..7 reduce w'_l for l = wib - 1, wib + 6, ... (fixed order over the CTAs)
+        for (int l = wib - 1; l >= 0 && l < jj; l += nwb - 1) {
+            double d = 0.0;
+            for (int b = lane; b < G; b += 32) d += __ldcg(a.pw + (long)b * (RQ_NB + 1) + l);
+            d = warp_sum(d);
+            if (lane == 0) wv[l] = d;
+        }
+        if (wib == 0 && lane == 0) red[0] = part;
+        for (int i = j + threadIdx.x; i < c; i += blockDim.x) ush[i] = __ldcg(a.ug + i);
+        __syncthreads();
+        part = red[0];
         const double x0 = ush[j];
         const double nrm = sqrt(part + x0 * x0);
         const double alpha = (x0 >= 0.0) ? -nrm : nrm;
@@ -495,14 +538,9 @@ rrqr3_kernel(Rrqr3Args a)
         __syncthreads();
         if (threadIdx.x == 0) ush[j] = v0;
         if (j == 0) r11 = fabs(alpha);
+        // w_l = V[j:, l]^T v = w'_l + V[j, l] v0
+        if (threadIdx.x < jj) wv[threadIdx.x] += a.V[(long)threadIdx.x * c + j] * v0;
         __syncthreads();
-        // w = V[j:, 0:jj]^T v (warp l handles l, l + 8, ...)
-        for (int l = wib; l < jj; l += nwb) {
-            double d = 0.0;
-            for (int i = j + lane; i < c; i += 32) d = fma(a.V[(long)l * c + i], ush[i], d);
-            d = warp_sum(d);
-            if (lane == 0) wv[l] = d;
-        }
         if (blockIdx.x == 0) {
             for (int i = threadIdx.x; i < c; i += blockDim.x) a.V[(long)jj * c + i] = (i >= j) ? ush[i] : 0.0;
             if (threadIdx.x == 0) {
@@ -520,7 +558,7 @@ rrqr3_kernel(Rrqr3Args a)
             if (!__shfl_sync(0xffffffffu, (int)m_act, t)) continue;
             const double *y = a.M + (long)col * c;
             double d = 0.0;
-#pragma unroll 8
+#pragma unroll 16
             for (int i = j + lane; i < c; i += 32) d = fma(y[i], ush[i], d);
             double *Fc = a.F + (long)col * RQ_NB;
             const double fl = (lane < jj) ? Fc[lane] : 0.0;
@@ -602,15 +640,17 @@ int RrqrWork::alloc(int nmax_, int cmax_) {
     LYAP_CUDA_TRY(cudaMalloc(&F3, sizeof(double) * (size_t)nmax * RQ_NB));
     LYAP_CUDA_TRY(cudaMalloc(&p3, sizeof(double) * (size_t)8 * p3_ctas));
     LYAP_CUDA_TRY(cudaMalloc(&st3, sizeof(double) * 4));
+    LYAP_CUDA_TRY(cudaMalloc(&ug3, sizeof(double) * (size_t)cmax));
+    LYAP_CUDA_TRY(cudaMalloc(&pw3, sizeof(double) * (size_t)p3_ctas * (RQ_NB + 1)));
     LYAP_CUDA_TRY(cudaMalloc(&act3, sizeof(int) * ((size_t)nmax + 8)));
     ist3 = act3 + nmax;
     return LYAP_OK;
 }
 void RrqrWork::release() {
-    for (double *p : {M, nrm, V3, F3, p3, st3}) if (p) cudaFree(p);
+    for (double *p : {M, nrm, V3, F3, p3, st3, ug3, pw3}) if (p) cudaFree(p);
     if (ints) cudaFree(ints);
     if (act3) cudaFree(act3);
-    M = nrm = scal = V3 = F3 = p3 = st3 = nullptr;
+    M = nrm = scal = V3 = F3 = p3 = st3 = ug3 = pw3 = nullptr;
     ints = act3 = ist3 = nullptr;
 }
 
@@ -648,7 +688,7 @@ static int rank_trunc_chol_blocked(cudaStream_t s, int n, int c, double tol, int
     for (;;) {
         Rrqr3Args a{n, c, kmax, j0, tol, w.M, w.V3, w.F3, w.p3, w.p3 + 2 * w.p3_ctas,
                     (int *)(w.p3 + 4 * w.p3_ctas), (int *)(w.p3 + 4 * w.p3_ctas) + 2 * w.p3_ctas,
-                    w.ints, w.act3, w.st3, ist};
+                    w.ints, w.act3, w.st3, ist, w.ug3, w.pw3};
         void *args[] = {&a};
         LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)rrqr3_kernel, dim3(grid), dim3(256), args, smem, s));
         LYAP_TRY(launched());

@@ -355,6 +355,12 @@ def _ir_parity(gpu, orc, p, us, ldlt, tol=1e-14, maxit=20, max_cols=256):
             ro = orc.ir_chol(p.A, p.L, us=us, tol=tol, imax=maxit)
     Xg, Xo = _X(res.Z, res.Y), _X(ro.Z, ro.Y)
     W = p.W()
+    # a reference independent of both precision models: the fp64 Bartels-Stewart solution
+    # (scipy), whose error is within kappa_Lyap x eps of the exact X
+    import scipy.linalg as sla
+    Xbs = sla.solve_continuous_lyapunov(p.A, -W)
+    if res.report["status"] == "converged":
+        assert np.linalg.norm(Xg - Xbs) <= 1e-10 * np.linalg.norm(Xbs)
     return res, ro, Xg, Xo, W
 
 
