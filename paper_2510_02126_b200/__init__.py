@@ -19,7 +19,8 @@ import os
 from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "liblyapir.so")
+# LYAP_LIB: an instrumented build (tools/ profiling runs only); default the in-tree library
+_LIB_PATH = os.environ.get("LYAP_LIB") or os.path.join(_HERE, "liblyapir.so")
 _lib = None
 
 FP64, FP32, FP16, BF16 = 0, 1, 2, 3

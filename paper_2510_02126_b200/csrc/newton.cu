@@ -16,6 +16,7 @@
 #include "lyap_internal.h"
 #include "newton_kernels.h"
 #include "ktimer.h"
+#include "ptx.cuh"
 
 namespace lyap {
 
@@ -313,6 +314,150 @@ newton_update_row_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ 
         dd = block_sum(dd, red); ss = block_sum(ss, red);     // block_sum's barriers also
         rs = block_sum(rs, red); mx = block_max(mx, red);     // free g for the next row
         if (threadIdx.x == 0) { part[4 * i] = dd; part[4 * i + 1] = ss; part[4 * i + 2] = rs; part[4 * i + 3] = mx; }
+    }
+}
+
+// The update as a persistent streaming kernel (round 2): one CTA per SM pair slot, rows
+// grid-strided.  invperm is staged ONCE per CTA as 16-bit indices; row i of G arrives by a
+// 1-D bulk async copy (cp.async.bulk, mbarrier completion) into one of two shared
+// buffers, the copy of row i + 2 grid being issued as soon as row i's buffer is free, so
+// the G stream never waits on the SM; the A_k row is loaded with all of a thread's
+// 16-byte vectors in flight before the wait.  Row partials: the sums ||A_{k+1} - A_k||_F^2
+// and ||A_{k+1}||_F^2 stay in per-thread registers across rows; the row abs-sum (for
+// ||A_{k+1} + I||_inf) is reduced per row through one parity-buffered warp slot and the
+// one barrier per row that also frees the G buffer.  part[4 b + 0..3] holds CTA b's
+// (sum dd, sum ss, max row sum, max |x|), reduced by reduce_rows_kernel over the grid.
+// Per-element arithmetic is newton_update_kernel's.  Traffic: A_k, G in, A_{k+1} out.
+template <typename T, int NT, int U>
+__global__ void __launch_bounds__(NT, 2)
+newton_update_stream_kernel(int n, const T *__restrict__ Ak, const T *__restrict__ G,
+                            const int *__restrict__ invperm, T *__restrict__ Anext,
+                            const double *__restrict__ scal, double *__restrict__ part)
+{
+    extern __shared__ __align__(128) unsigned char nus_smem[];
+    constexpr int NW = NT / 32;
+    constexpr int V = 16 / sizeof(T);
+    using Acc = typename Prec<T>::acc;
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(nus_smem);
+    T *const gbuf0 = reinterpret_cast<T *>(nus_smem + 128);
+    uint16_t *ip = reinterpret_cast<uint16_t *>(gbuf0 + 2 * (long)n);
+    __shared__ double wred[2][NW];
+    __shared__ double red[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int grid = gridDim.x, nv = n / V;
+    const uint32_t rowbytes = (uint32_t)n * sizeof(T);
+    const double mu = scal[SC_MU];
+    const int e = (int)scal[SC_EXP];
+    const Acc a = (Acc)mu, b = (Acc)(1.0 / mu);
+    const float scf = ldexpf(1.0f, -e);
+    const double scd = ldexp(1.0, -e);
+    if (tid == 0) {
+        ptx::mbar_init(&mbar[0], 1);
+        ptx::mbar_init(&mbar[1], 1);
+        ptx::fence_mbar_init();
+        for (int t = 0; t < 2; t++) {
+            const int i = blockIdx.x + t * grid;
+            if (i < n) {
+                ptx::mbar_arrive_expect_tx(&mbar[t], rowbytes);
+                ptx::bulk_g2s(gbuf0 + (long)t * n, G + (long)i * n, rowbytes, &mbar[t]);
+            }
+        }
+    }
+    for (int j = tid; j < n; j += NT) ip[j] = (uint16_t)invperm[j];
+    __syncthreads();
+    double dd = 0.0, ss = 0.0, mx = 0.0, rsmax = 0.0;
+    int t = 0;
+    for (int i = blockIdx.x; i < n; i += grid, t++) {
+        const int bsel = t & 1;
+        const uint32_t parity = (uint32_t)(t >> 1) & 1u;
+        const uint4 *Ai = reinterpret_cast<const uint4 *>(Ak + (long)i * n);
+        uint4 *Ni = reinterpret_cast<uint4 *>(Anext + (long)i * n);
+        const T *g = gbuf0 + (long)bsel * n;
+        double rs = 0.0;
+        for (int base = 0; base < nv; base += NT * U) {
+            uint4 av[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int jv = base + u * NT + tid;
+                if (jv < nv) av[u] = __ldcs(Ai + jv);
+            }
+            if (base == 0) ptx::mbar_wait(&mbar[bsel], parity);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int jv = base + u * NT + tid;
+                if (jv >= nv) continue;
+                const T *ae = reinterpret_cast<const T *>(&av[u]);
+                uint4 nw;
+                T *ne = reinterpret_cast<T *>(&nw);
+                uint16_t idx[V];
+                if constexpr (V == 8) {
+                    const uint4 iv = reinterpret_cast<const uint4 *>(ip)[jv];
+                    const uint32_t w4[4] = {iv.x, iv.y, iv.z, iv.w};
+#pragma unroll
+                    for (int q = 0; q < 4; q++) { idx[2 * q] = (uint16_t)(w4[q] & 0xFFFFu); idx[2 * q + 1] = (uint16_t)(w4[q] >> 16); }
+                } else if constexpr (V == 4) {
+                    const uint2 iv = reinterpret_cast<const uint2 *>(ip)[jv];
+                    idx[0] = (uint16_t)(iv.x & 0xFFFFu); idx[1] = (uint16_t)(iv.x >> 16);
+                    idx[2] = (uint16_t)(iv.y & 0xFFFFu); idx[3] = (uint16_t)(iv.y >> 16);
+                } else {
+                    const uint32_t iv = reinterpret_cast<const uint32_t *>(ip)[jv];
+                    idx[0] = (uint16_t)(iv & 0xFFFFu); idx[1] = (uint16_t)(iv >> 16);
+                }
+                float ddf = 0.f, ssf = 0.f, rsf = 0.f, mxf = 0.f;
+#pragma unroll
+                for (int q = 0; q < V; q++) {
+                    const int j = jv * V + q;
+                    T gi;
+                    if constexpr (sizeof(T) == 8) gi = g[idx[q]] * scd;
+                    else gi = from_f<T>(to_f<T>(g[idx[q]]) * scf);
+                    const Acc x = to_acc<T>(ae[q]);
+                    const Acc y = to_acc<T>(gi);
+                    const T nvt = from_acc<T>(Acc(0.5) * fma(a, x, b * y));
+                    ne[q] = nvt;
+                    if constexpr (sizeof(T) == 2) {
+                        const float nd = to_f<T>(nvt), df = nd - (float)x;
+                        ddf = fmaf(df, df, ddf);
+                        ssf = fmaf(nd, nd, ssf);
+                        rsf += fabsf(nd + (i == j ? 1.0f : 0.0f));
+                        mxf = fmaxf(mxf, fabsf(nd));
+                        if (!isfinite(nd)) mxf = INFINITY;
+                    } else {
+                        const double nd = to_d<T>(nvt), xd = (double)x;
+                        dd = fma(nd - xd, nd - xd, dd);
+                        ss = fma(nd, nd, ss);
+                        rs += fabs(nd + (i == j ? 1.0 : 0.0));
+                        mx = fmax(mx, fabs(nd));
+                        if (!isfinite(nd)) mx = INFINITY;
+                    }
+                }
+                if constexpr (sizeof(T) == 2) {
+                    dd += (double)ddf; ss += (double)ssf; rs += (double)rsf;
+                    mx = fmax(mx, (double)mxf);
+                }
+                __stcs(Ni + jv, nw);
+            }
+        }
+        rs = warp_sum(rs);
+        if (lane == 0) wred[bsel][wid] = rs;
+        __syncthreads();                       // G buffer bsel free, wred[bsel] complete
+        if (tid == 0) {
+            double r = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; w++) r += wred[bsel][w];
+            rsmax = fmax(rsmax, r);
+            const int inext = i + 2 * grid;
+            if (inext < n) {
+                ptx::mbar_arrive_expect_tx(&mbar[bsel], rowbytes);
+                ptx::bulk_g2s(gbuf0 + (long)bsel * n, G + (long)inext * n, rowbytes, &mbar[bsel]);
+            }
+        }
+    }
+    dd = block_sum(dd, red);
+    ss = block_sum(ss, red);
+    mx = block_max(mx, red);
+    if (tid == 0) {
+        part[4 * blockIdx.x] = dd; part[4 * blockIdx.x + 1] = ss;
+        part[4 * blockIdx.x + 2] = rsmax; part[4 * blockIdx.x + 3] = mx;
     }
 }
 
@@ -662,42 +807,78 @@ int nk_mu_det(cudaStream_t s, int n, const double *ldet, double *scal, int scali
     return launched();
 }
 
-// Row-staged form when a row of G fits the shared-memory budget and rows are 16-byte
-// multiples; grid = resident CTAs per SM x SMs (rows are grid-strided).
+// Launch forms of the update, by preference: the persistent streaming kernel (rows of
+// 16-byte multiples, two G rows + 16-bit invperm in shared memory, n < 65536, no
+// un-permuted copy requested); the row-staged kernel; the plain kernel.  Returns the
+// number of partial rows written to part.
 static constexpr int NU_SMEM_MAX = 96 * 1024;
-template <typename T> static void k_update(cudaStream_t s, int n, const void *Ak, const void *G, const int *ip,
-                                           void *An, void *Ai, const double *scal, double *part)
+static constexpr int NUS_NT = 512, NUS_U = 4;
+static int sm_count() {
+    static const int v = [] {
+        int dev = 0, c = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+        return c;
+    }();
+    return v;
+}
+template <typename T> static int k_update(cudaStream_t s, int n, const void *Ak, const void *G, const int *ip,
+                                          void *An, void *Ai, const double *scal, double *part)
 {
-    const size_t smem = (size_t)n * sizeof(T);
-    if (n % (16 / (int)sizeof(T)) == 0 && smem <= (size_t)NU_SMEM_MAX) {
-        static const int nsm = [] {
-            cudaFuncSetAttribute(newton_update_row_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, NU_SMEM_MAX);
-            int dev = 0, v = 148;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-            return v;
+    constexpr int V = 16 / (int)sizeof(T);
+    const size_t smem_s = 128 + 2 * (size_t)n * sizeof(T) + 2 * (size_t)n;
+    if (!Ai && n % V == 0 && n < 65536 && smem_s <= 200 * 1024 && !env_flag("LYAP_NU_ROW")) {
+        static const bool attr = [] {
+            cudaFuncSetAttribute(newton_update_stream_kernel<T, NUS_NT, NUS_U>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            return true;
         }();
+        (void)attr;
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, newton_update_stream_kernel<T, NUS_NT, NUS_U>, NUS_NT,
+                                                      smem_s);
+        per_sm = std::max(1, std::min(per_sm, 2));
+        const int grid = std::min(n, sm_count() * per_sm);
+        newton_update_stream_kernel<T, NUS_NT, NUS_U><<<grid, NUS_NT, smem_s, s>>>(
+            n, (const T *)Ak, (const T *)G, ip, (T *)An, scal, part);
+        return grid;
+    }
+    const size_t smem = (size_t)n * sizeof(T);
+    if (n % V == 0 && smem <= (size_t)NU_SMEM_MAX) {
+        static const bool attr = [] {
+            cudaFuncSetAttribute(newton_update_row_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, NU_SMEM_MAX);
+            return true;
+        }();
+        (void)attr;
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, newton_update_row_kernel<T>, 256, smem);
         if (per_sm < 1) per_sm = 1;
-        const int grid = n < nsm * per_sm ? n : nsm * per_sm;
+        const int grid = n < sm_count() * per_sm ? n : sm_count() * per_sm;
         newton_update_row_kernel<T><<<grid, 256, smem, s>>>(n, (const T *)Ak, (const T *)G, ip, (T *)An, (T *)Ai,
                                                              scal, part);
-        return;
+        return n;
     }
     newton_update_kernel<T><<<n < 4096 ? n : 4096, 256, 0, s>>>(n, (const T *)Ak, (const T *)G, ip, (T *)An, (T *)Ai, scal, part);
+    return n;
 }
 int nk_update(cudaStream_t s, int prec, int n, const void *Ak, const void *G, const int *invperm, void *Anext,
               void *Ainv, double *scal, double *part)
 {
+    int rows = n;
     {
         const double es = prec == LYAP_FP64 ? 8.0 : prec == LYAP_FP32 ? 4.0 : 2.0;
         // algorithmic bytes: A_k and G in, A_{k+1} out (+ the cached A_k^{-1} if requested)
         KTimer kt(KC_NEWTON_UPDATE, s, 0.0, (Ainv ? 4.0 : 3.0) * es * (double)n * n);
-        DISPATCH_T(prec, k_update, s, n, Ak, G, invperm, Anext, Ainv, scal, part);
+        switch (prec) {
+            case LYAP_FP64: rows = k_update<double>(s, n, Ak, G, invperm, Anext, Ainv, scal, part); break;
+            case LYAP_FP32: rows = k_update<float>(s, n, Ak, G, invperm, Anext, Ainv, scal, part); break;
+            case LYAP_FP16: rows = k_update<__half>(s, n, Ak, G, invperm, Anext, Ainv, scal, part); break;
+            case LYAP_BF16: rows = k_update<__nv_bfloat16>(s, n, Ak, G, invperm, Anext, Ainv, scal, part); break;
+            default: return LYAP_ERR_ARG;
+        }
     }
     LYAP_TRY(launched());
-    reduce_rows_kernel<<<1, 1024, 0, s>>>(n, part, scal + SC_RED);
+    reduce_rows_kernel<<<1, 1024, 0, s>>>(rows, part, scal + SC_RED);
     return launched();
 }
 
