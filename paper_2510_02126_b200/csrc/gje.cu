@@ -128,8 +128,8 @@ gje_panel_kernel(int n, int k, int b, T *__restrict__ A, T *__restrict__ X,
         for (int i = b - 1; i >= 0; i--) {
             Acc s = (i == c) ? Acc(1) : Acc(0);
             if (i < c)
-                for (int t = i + 1; t <= c; t++) s = fma(-P[(long)i * b + t], Uw[t * 32 + c], s);
-            Uw[i * 32 + c] = (i > c) ? Acc(0) : s / P[(long)i * b + i];
+                for (int t = c; t >= i + 1; t--) s = fma(-P[(long)i * b + t], Uw[t * 32 + c], s);   // newest x last: short chain
+            Uw[i * 32 + c] = (i > c) ? Acc(0) : s * (Acc(1) / P[(long)i * b + i]);   // reciprocal: off the chain
         }
     }
     __syncthreads();
@@ -501,9 +501,9 @@ gje_panel_cluster_kernel(int n, int k, int b, int RB, const T *__restrict__ A, T
             for (int i = b - 1; i >= 0; i--) {
                 Acc sacc = (i == c) ? Acc(1) : Acc(0);
 #pragma unroll
-                for (int t = 1; t < BW; t++)
+                for (int t = BW - 1; t >= 1; t--)                // descending: x_{i+1}, the newest, enters last
                     if (t >= i + 1 && t <= c) sacc = fma(-Ptop[i][t], Uw[t * 32 + c], sacc);
-                Uw[i * 32 + c] = (i > c) ? Acc(0) : sacc / Ptop[i][i];
+                Uw[i * 32 + c] = (i > c) ? Acc(0) : sacc * (Acc(1) / Ptop[i][i]);   // reciprocal: off the chain
             }
         } else if (tid >= 64 && tid < 96) {
             // moved rows: replay the transpositions on the candidate positions (one warp)
@@ -1108,9 +1108,14 @@ extern "C" int lyap_invert(int n, int prec, void *A, int *ipiv, void *stream)
     void *out = nullptr;
     int rc = LYAP_OK;
     if (cudaMalloc(&out, elem_size(prec) * (size_t)n * n) != cudaSuccess) { w.release(); return LYAP_ERR_CUDA; }
-    rc = gje_invert(s, n, prec, A, w);
-    if (rc == LYAP_OK) rc = col_gather(s, n, prec, A, w.invperm, out);
-    if (rc == LYAP_OK && cudaMemcpyAsync(A, out, elem_size(prec) * (size_t)n * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) rc = LYAP_ERR_CUDA;
+    if (gje_ip_eligible(n, prec, w)) {
+        rc = gje_ip_invert(s, n, prec, A, out, w);
+        if (rc == LYAP_OK) rc = col_gather(s, n, prec, out, w.invperm, A);
+    } else {
+        rc = gje_invert(s, n, prec, A, w);
+        if (rc == LYAP_OK) rc = col_gather(s, n, prec, A, w.invperm, out);
+        if (rc == LYAP_OK && cudaMemcpyAsync(A, out, elem_size(prec) * (size_t)n * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) rc = LYAP_ERR_CUDA;
+    }
     if (rc == LYAP_OK && ipiv && cudaMemcpyAsync(ipiv, w.ipiv, sizeof(int) * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) rc = LYAP_ERR_CUDA;
     int info = 0;
     if (rc == LYAP_OK && cudaMemcpyAsync(&info, w.info, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = LYAP_ERR_CUDA;

@@ -149,9 +149,16 @@ int aseq_compute(lyap_ir_ctx *h, const double *A) {
         if ((int)h->iexp.size() < it) h->iexp.push_back(0);
         // W = 2^{-e} A_k goes straight into the cache slot and is inverted in place there
         // (the Newton update then streams A_k and G in and A_{k+1} out: three n^2 streams)
+        // (the implicit-pivoting sweep works in the free A_{k+1} buffer and writes its result,
+        // rows back in order, into the slot)
         void *G = h->inv[it - 1];
-        LYAP_TRY(nk_scale(s, us, nn, h->Ak, G, h->scal));
-        LYAP_TRY(gje_invert(s, n, us, G, h->gje));
+        if (gje_ip_eligible(n, us, h->gje)) {
+            LYAP_TRY(nk_scale(s, us, nn, h->Ak, h->An, h->scal));
+            LYAP_TRY(gje_ip_invert(s, n, us, h->An, G, h->gje));
+        } else {
+            LYAP_TRY(nk_scale(s, us, nn, h->Ak, G, h->scal));
+            LYAP_TRY(gje_invert(s, n, us, G, h->gje));
+        }
         // mu_k: Frobenius-norm scaling (opt.scaling = 1, the paper's choice l.1406) or
         // determinantal scaling |det A_k|^{-1/n} (opt.scaling = 2, l.1139)
         if (h->opt.scaling == 2) LYAP_TRY(nk_mu_det(s, n, h->gje.ldet, h->scal, scaling_on));

@@ -22,6 +22,9 @@ struct GjeWork {
 };
 
 int gje_invert(cudaStream_t s, int n, int prec, void *A, GjeWork &w);
+// implicit-pivoting sweep (gje_ip.cu): A is destroyed, the result (gje_invert's layout) goes to G != A
+bool gje_ip_eligible(int n, int prec, const GjeWork &w);
+int gje_ip_invert(cudaStream_t s, int n, int prec, void *A, void *G, GjeWork &w);
 // LYAP_GEMM=simt routes the 16-bit products through the SIMT kernel (cross-checking)
 inline bool use_simt_gemm() {
     static int v = -1;

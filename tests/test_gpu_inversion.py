@@ -163,3 +163,44 @@ def test_newton_cached_inverses_vs_oracle(gpu, orc, us):
         print(f"{us} cached inverse {j}: {err:.3e} = {err / (u * k2):.3f} u kappa_2")
         assert err <= max(2 * C_INV * u * k2 * (j + 1), 1e-13)   # measured max 5.4 (fp64, j = 4)
         assert err < 0.5
+
+
+@pytest.mark.parametrize("us", ["fp16", "bf16", "fp32"])
+@pytest.mark.parametrize("n", [1024, 2048, 4096])
+def test_implicit_pivoting_equals_row_swapping(gpu, us, n, monkeypatch):
+    """The implicit-pivoting sweep (gje_ip.cu: rows stay in place, positions are exchanged;
+    cluster panel with st.async candidate pushes) against the row-swapping sweep (gje.cu,
+    LYAP_GJE_SWAP=1): the same LU-with-partial-pivoting pivot sequence (ties by the lowest
+    position) and the same arithmetic on every element, so the inverses are equal bit for
+    bit (one inversion per Newton step; north_star: partial pivoting)."""
+    A = torch.as_tensor(_test_matrix(n, 64.0, seed=5 * n), dtype=torch.float64, device="cuda").to(TDT[us]).contiguous()
+    X1, p1 = A.clone(), torch.zeros(n, dtype=torch.int32, device="cuda")
+    monkeypatch.delenv("LYAP_GJE_SWAP", raising=False)
+    gpu.invert(X1, p1)
+    X2, p2 = A.clone(), torch.zeros(n, dtype=torch.int32, device="cuda")
+    monkeypatch.setenv("LYAP_GJE_SWAP", "1")
+    gpu.invert(X2, p2)
+    torch.cuda.synchronize()
+    assert torch.equal(p1, p2)
+    assert torch.equal(X1, X2)
+    res = (A.double() @ X1.double() - torch.eye(n, device="cuda", dtype=torch.float64)).norm() / n ** 0.5
+    assert float(res) < 0.05
+
+
+def test_implicit_pivoting_ties_and_zeros(gpu, monkeypatch):
+    """A matrix with many equal-magnitude pivot candidates and exact zeros (the convection-
+    diffusion stencil of configs[2], n = 32 x 32 grid): the tie rule (lowest logical position)
+    must reproduce the row-swapping sweep's pivots exactly."""
+    p = P.cfg2(g=32)
+    A = torch.as_tensor(p.A, dtype=torch.float64, device="cuda")
+    A = (A / A.abs().max()).to(torch.float16).contiguous()
+    n = A.shape[0]
+    X1, p1 = A.clone(), torch.zeros(n, dtype=torch.int32, device="cuda")
+    monkeypatch.delenv("LYAP_GJE_SWAP", raising=False)
+    gpu.invert(X1, p1)
+    X2, p2 = A.clone(), torch.zeros(n, dtype=torch.int32, device="cuda")
+    monkeypatch.setenv("LYAP_GJE_SWAP", "1")
+    gpu.invert(X2, p2)
+    torch.cuda.synchronize()
+    assert torch.equal(p1, p2)
+    assert torch.equal(X1, X2)
