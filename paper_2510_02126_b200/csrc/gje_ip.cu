@@ -587,40 +587,44 @@ gje_ip_x_kernel(int n, int k, T *__restrict__ A, const int *__restrict__ pos_g, 
 }
 
 // Outer step: the nb pivot rows' entries outside the block columns go to Bo (K-major:
-// Bo[c][y], transposed through shared memory) and are zeroed.
+// Bo[c][y]) and are zeroed.  One CTA per tile of 64 columns x 128 pivot rows: 16-byte loads
+// along the rows, transposed through shared memory, 16-byte stores along y.
 template <typename T>
 __global__ void __launch_bounds__(256)
 gje_ip_outer_prep_kernel(int n, int K0, int nb, T *__restrict__ A, const int *__restrict__ piv, T *__restrict__ Bo)
 {
-    __shared__ T tile[32][33];
-    __shared__ int prow[GJE_NB];
-    for (int y = threadIdx.x; y < nb; y += blockDim.x) prow[y] = piv[K0 + y];
-    __syncthreads();
+    constexpr int VE = 16 / (int)sizeof(T);                       // elements per 16-byte vector
+    constexpr int TC = 64, TR = 128;                              // tile: columns x pivot rows
+    __shared__ T tile[TR][TC + VE];                               // row stride keeps 16-byte alignment
+    __shared__ int prow[TR];
     const int nrest = n - nb;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;      // 32 x 8
-    const T zero = from_acc<T>(0.f);
-    for (int e0 = blockIdx.x * 32; e0 < nrest; e0 += gridDim.x * 32) {
-        for (int y0 = 0; y0 < nb; y0 += 32) {
-            for (int yy = ty; yy < 32; yy += 8) {
-                const int y = y0 + yy, e = e0 + tx;
-                T v = zero;
-                if (y < nb && e < nrest) {
-                    const int c = e < K0 ? e : e + nb;
-                    T *ap = A + (long)prow[y] * n + c;
-                    v = *ap;
-                    *ap = zero;
-                }
-                tile[yy][tx] = v;
-            }
-            __syncthreads();
-            for (int cc = ty; cc < 32; cc += 8) {
-                const int e = e0 + cc, y = y0 + tx;
-                if (e < nrest && y < nb) {
-                    const int c = e < K0 ? e : e + nb;
-                    Bo[(long)c * nb + y] = tile[tx][cc];
-                }
-            }
-            __syncthreads();
+    const int e0 = blockIdx.x * TC, y0 = blockIdx.y * TR;
+    for (int y = threadIdx.x; y < TR; y += blockDim.x) prow[y] = (y0 + y < nb) ? piv[K0 + y0 + y] : -1;
+    __syncthreads();
+    // rest column e -> matrix column c (the block columns are skipped); K0 and nb are
+    // multiples of VE, so a vector never straddles the block
+    constexpr int CV = TC / VE;                                   // vectors per tile row
+    for (int idx = threadIdx.x; idx < TR * CV; idx += blockDim.x) {
+        const int yy = idx / CV, cv = idx - yy * CV, e = e0 + cv * VE;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (prow[yy] >= 0 && e < nrest) {
+            const int c = e < K0 ? e : e + nb;
+            uint4 *ap = reinterpret_cast<uint4 *>(A + (long)prow[yy] * n + c);
+            v = *ap;
+            *ap = make_uint4(0u, 0u, 0u, 0u);
+        }
+        *reinterpret_cast<uint4 *>(&tile[yy][cv * VE]) = v;
+    }
+    __syncthreads();
+    constexpr int YV = TR / VE;                                   // y-vectors per tile column
+    for (int idx = threadIdx.x; idx < TC * YV; idx += blockDim.x) {
+        const int cc = idx / YV, yv = idx - cc * YV, e = e0 + cc, y = y0 + yv * VE;
+        if (e < nrest && y < nb) {
+            alignas(16) T o[VE];
+#pragma unroll
+            for (int u = 0; u < VE; u++) o[u] = tile[yv * VE + u][cc];
+            const int c = e < K0 ? e : e + nb;
+            *reinterpret_cast<uint4 *>(Bo + (long)c * nb + y) = *reinterpret_cast<const uint4 *>(o);
         }
     }
 }
@@ -644,12 +648,12 @@ __global__ void iota2_kernel(int n, int *a, int *b) {
 }
 
 template <typename T>
-int ip_gemm(cudaStream_t s, int M, int N, int K, const T *A, long lda, const T *B, long ldb, T *C, long ldc)
+int ip_gemm(cudaStream_t s, int M, int N, int K, const T *A, long lda, const T *B, long ldb, T *C, long ldc, int cap = 0)
 {
     if constexpr (std::is_same<T, float>::value)
         return gemm_strided<float, float, float, float>(s, M, N, K, 1.0f, A, lda, 1, B, 1, ldb, 1.0f, C, ldc, 1);
     else
-        return tc_gemm(s, Prec<T>::code, M, N, K, 1.0f, A, lda, B, ldb, 1.0f, C, ldc, 0, 0);
+        return tc_gemm(s, Prec<T>::code, M, N, K, 1.0f, A, lda, B, ldb, 1.0f, C, ldc, 0, cap);
 }
 
 template <typename T, int NT, int RPT, bool XOUT>
@@ -701,29 +705,52 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
     if (const char *e = getenv("LYAP_GJE_IP_RPT")) rpt = atoi(e);
     if (ceil_div(n, nt * rpt) > 16) { nt = n <= 8192 ? 512 : 1024; rpt = 1; }
     const bool xout = !env_flag("LYAP_GJE_IP_XIN");             // 512-thread panels: X rows by the separate kernel
+    // Look-ahead: the panels and rank-32 updates of block K0 + NB run on the high-priority
+    // stream P while the main stream applies the rest of block K0's rank-NB update.  Order on
+    // the main stream: B_outer, the update of the NEXT block's columns (then P may start), the
+    // update of all other columns as one CTA per tile -- SMs come free tile by tile, so P's
+    // cluster launches are not locked out.  The two streams touch disjoint columns of A.
+    const bool ahead = w.side != nullptr && n >= 4 * GJE_NB && !env_flag("LYAP_GJE_NO_LOOKAHEAD");
+    cudaStream_t P = ahead ? w.side : s;
+    if (ahead) {
+        LYAP_CUDA_TRY(cudaEventRecord(w.ev_a, s));
+        LYAP_CUDA_TRY(cudaStreamWaitEvent(P, w.ev_a, 0));
+    }
     for (int K0 = 0; K0 < n; K0 += GJE_NB) {
         const int nbk = std::min(GJE_NB, n - K0);
         for (int k = K0; k < K0 + nbk; k += BW) {
             {
-                KTimer kt(KC_GJE_PANEL, s, (double)(n - k) * BW * BW + 2.0 * n * BW * BW,
+                KTimer kt(KC_GJE_PANEL, P, (double)(n - k) * BW * BW + 2.0 * n * BW * BW,
                           (double)sizeof(T) * ((double)n * BW + (double)n * BW));
-                if (nt == 256 && rpt == 1) LYAP_TRY(panel_launch<T, 256, 1, false>(s, n, k, K0, nbk, A, w));
-                else if (nt == 256) LYAP_TRY(panel_launch<T, 256, 2, false>(s, n, k, K0, nbk, A, w));
-                else if (nt == 512 && rpt == 1 && !xout) LYAP_TRY(panel_launch<T, 512, 1, false>(s, n, k, K0, nbk, A, w));
-                else if (nt == 512 && rpt == 1) LYAP_TRY(panel_launch<T, 512, 1, true>(s, n, k, K0, nbk, A, w));
-                else if (nt == 512) LYAP_TRY(panel_launch<T, 512, 2, true>(s, n, k, K0, nbk, A, w));
-                else LYAP_TRY(panel_launch<T, 1024, 1, true>(s, n, k, K0, nbk, A, w));
+                if (nt == 256 && rpt == 1) LYAP_TRY(panel_launch<T, 256, 1, false>(P, n, k, K0, nbk, A, w));
+                else if (nt == 256) LYAP_TRY(panel_launch<T, 256, 2, false>(P, n, k, K0, nbk, A, w));
+                else if (nt == 512 && rpt == 1 && !xout) LYAP_TRY(panel_launch<T, 512, 1, false>(P, n, k, K0, nbk, A, w));
+                else if (nt == 512 && rpt == 1) LYAP_TRY(panel_launch<T, 512, 1, true>(P, n, k, K0, nbk, A, w));
+                else if (nt == 512) LYAP_TRY(panel_launch<T, 512, 2, true>(P, n, k, K0, nbk, A, w));
+                else LYAP_TRY(panel_launch<T, 1024, 1, true>(P, n, k, K0, nbk, A, w));
             }
-            KTimer kt(KC_GJE_UPDATE, s);
-            LYAP_TRY(ip_gemm<T>(s, n, nbk, BW, (const T *)w.X, BW, (const T *)w.B + (size_t)K0 * BW, BW, A + K0, n));
+            KTimer kt(KC_GJE_UPDATE, P);
+            LYAP_TRY(ip_gemm<T>(P, n, nbk, BW, (const T *)w.X, BW, (const T *)w.B + (size_t)K0 * BW, BW, A + K0, n));
+        }
+        if (ahead) {
+            LYAP_CUDA_TRY(cudaEventRecord(w.ev_b, P));             // inner steps of this block done
+            LYAP_CUDA_TRY(cudaStreamWaitEvent(s, w.ev_b, 0));
         }
         if (n - nbk > 0) {
-            gje_ip_outer_prep_kernel<T><<<std::min(ceil_div(n - nbk, 32), 592), 256, 0, s>>>(n, K0, nbk, A, w.rowperm, (T *)w.Bo);
+            gje_ip_outer_prep_kernel<T><<<dim3(ceil_div(n - nbk, 64), ceil_div(nbk, 128)), 256, 0, s>>>(n, K0, nbk, A, w.rowperm, (T *)w.Bo);
             LYAP_TRY(launched());
             KTimer kt(KC_GJE_UPDATE, s);
-            if (K0 > 0) LYAP_TRY(ip_gemm<T>(s, n, K0, nbk, A + K0, n, (const T *)w.Bo, nbk, A, n));
             const int cr = K0 + nbk;
-            if (cr < n) LYAP_TRY(ip_gemm<T>(s, n, n - cr, nbk, A + K0, n, (const T *)w.Bo + (size_t)cr * nbk, nbk, A + cr, n));
+            const int cn = ahead ? std::min(n, cr + GJE_NB) : cr;
+            if (ahead && cn > cr) {
+                LYAP_TRY(ip_gemm<T>(s, n, cn - cr, nbk, A + K0, n, (const T *)w.Bo + (size_t)cr * nbk, nbk, A + cr, n));
+                LYAP_CUDA_TRY(cudaEventRecord(w.ev_a, s));
+                LYAP_CUDA_TRY(cudaStreamWaitEvent(P, w.ev_a, 0));
+            }
+            int cap = (ahead && cn > cr) ? -1 : 0;
+            if (const char *e = getenv("LYAP_GJE_LA_CAP")) cap = (ahead && cn > cr) ? atoi(e) : 0;   // tuning
+            if (K0 > 0) LYAP_TRY(ip_gemm<T>(s, n, K0, nbk, A + K0, n, (const T *)w.Bo, nbk, A, n, cap));
+            if (cn < n) LYAP_TRY(ip_gemm<T>(s, n, n - cn, nbk, A + K0, n, (const T *)w.Bo + (size_t)cn * nbk, nbk, A + cn, n, cap));
         }
     }
     gje_ip_finish_kernel<T><<<std::min(n, 148 * 8), 256, 0, s>>>(n, A, w.rowperm, G);

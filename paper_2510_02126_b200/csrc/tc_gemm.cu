@@ -474,7 +474,9 @@ int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const vo
     }();
     KTimer kt(KC_TCGEMM, s, 2.0 * M * N * K, 2.0 * ((double)M * K + (double)N * K + (beta != 0.f ? 2.0 : 1.0) * M * N));
     const int tiles = (int)(grid.x * grid.y);
-    if (ctma && tiles >= nsm && !env_flag("LYAP_TC_NONPERSISTENT")) {
+    // max_ctas < 0: one CTA per tile (SMs come free tile by tile, so a concurrent
+    // high-priority cluster launch is not locked out for the whole product)
+    if (ctma && tiles >= nsm && max_ctas >= 0 && !env_flag("LYAP_TC_NONPERSISTENT")) {
         const int g = std::min(tiles, max_ctas > 0 ? std::min(max_ctas, nsm) : nsm);
         if (prec == LYAP_BF16)
             tc_gemm_persistent_kernel<__nv_bfloat16><<<g, tc::PTHREADS, tc::PSMEM, s>>>(ma, mb, mc, M, N, K, alpha, beta);
