@@ -479,17 +479,29 @@ def sign_newton_scale(G, P, dev, pk, which):
     res = {"workload": f"{which}: n={n} fp16 sign-Newton A-sequence ({k} inversions)", "ms": ms,
            "tflops": flops / (ms / 1e3) / 1e12}
     res["frac_of_fp16_peak"] = res["tflops"] / pk["bf16"]
+    # per-class event times with the look-ahead stream off: with it the rank-512 update runs
+    # beside the next block's panels, and events around a launch would time both
     classes = {}
-    for name in ("tc_gemm", "gje_panel", "gje_update"):
-        G.kernel_timing(name)
+    os.environ["LYAP_GJE_NO_LOOKAHEAD"] = "1"
+    try:
+        e0.record()
         s.newton_aseq(A)
-        classes[name] = G.kernel_stats()
-    G.kernel_timing(None)
+        e1.record()
+        torch.cuda.synchronize()
+        res["ms_without_lookahead"] = e0.elapsed_time(e1)
+        for name in ("tc_gemm", "gje_panel", "gje_update"):
+            G.kernel_timing(name)
+            s.newton_aseq(A)
+            classes[name] = G.kernel_stats()
+        G.kernel_timing(None)
+    finally:
+        os.environ.pop("LYAP_GJE_NO_LOOKAHEAD", None)
     ms_t, cnt, fl, _ = classes["tc_gemm"]
     ach = fl / (ms_t / 1e3) / 1e12 if ms_t > 0 else 0.0
     res["tc_gemm"] = {"bound": "tensor", "achieved": ach, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
                       "frac": ach / pk["bf16_sus"], "launches": cnt, "ms": ms_t}
     res["class_ms"] = {k2: v[0] for k2, v in classes.items()}
+    res["class_ms_note"] = "serial order (LYAP_GJE_NO_LOOKAHEAD=1); gje_panel = pivot panels + X rows, gje_update = all update GEMMs"
     # the fused Newton averaging update (HBM-streaming: read A_k and the inverse, write
     # A_{k+1} and the cached A_k^{-1}: 4 x 2 n^2 bytes per launch in fp16)
     G.kernel_timing("newton_update")

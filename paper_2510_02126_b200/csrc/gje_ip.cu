@@ -604,16 +604,26 @@ gje_ip_outer_prep_kernel(int n, int K0, int nb, T *__restrict__ A, const int *__
     // rest column e -> matrix column c (the block columns are skipped); K0 and nb are
     // multiples of VE, so a vector never straddles the block
     constexpr int CV = TC / VE;                                   // vectors per tile row
-    for (int idx = threadIdx.x; idx < TR * CV; idx += blockDim.x) {
-        const int yy = idx / CV, cv = idx - yy * CV, e = e0 + cv * VE;
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    constexpr int NI = TR * CV / 256;                             // vectors per thread: all loads first
+    static_assert(TR * CV % 256 == 0, "tile / block size");
+    uint4 v[NI];
+    uint4 *ap[NI];
+#pragma unroll
+    for (int i = 0; i < NI; i++) {
+        const int idx = threadIdx.x + i * 256, yy = idx / CV, cv = idx - yy * CV, e = e0 + cv * VE;
+        ap[i] = nullptr;
+        v[i] = make_uint4(0u, 0u, 0u, 0u);
         if (prow[yy] >= 0 && e < nrest) {
             const int c = e < K0 ? e : e + nb;
-            uint4 *ap = reinterpret_cast<uint4 *>(A + (long)prow[yy] * n + c);
-            v = *ap;
-            *ap = make_uint4(0u, 0u, 0u, 0u);
+            ap[i] = reinterpret_cast<uint4 *>(A + (long)prow[yy] * n + c);
+            v[i] = *ap[i];
         }
-        *reinterpret_cast<uint4 *>(&tile[yy][cv * VE]) = v;
+    }
+#pragma unroll
+    for (int i = 0; i < NI; i++) {
+        const int idx = threadIdx.x + i * 256, yy = idx / CV, cv = idx - yy * CV;
+        if (ap[i]) *ap[i] = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4 *>(&tile[yy][cv * VE]) = v[i];
     }
     __syncthreads();
     constexpr int YV = TR / VE;                                   // y-vectors per tile column
@@ -703,6 +713,7 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
     int nt = n <= 4096 ? 256 : 512, rpt = n <= 8192 ? 1 : 2;
     if (const char *e = getenv("LYAP_GJE_IP_NT")) nt = atoi(e);
     if (const char *e = getenv("LYAP_GJE_IP_RPT")) rpt = atoi(e);
+    if (nt == 128) rpt = 2;
     if (ceil_div(n, nt * rpt) > 16) { nt = n <= 8192 ? 512 : 1024; rpt = 1; }
     const bool xout = !env_flag("LYAP_GJE_IP_XIN");             // 512-thread panels: X rows by the separate kernel
     // Look-ahead: the panels and rank-32 updates of block K0 + NB run on the high-priority
@@ -710,6 +721,9 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
     // the main stream: B_outer, the update of the NEXT block's columns (then P may start), the
     // update of all other columns as one CTA per tile -- SMs come free tile by tile, so P's
     // cluster launches are not locked out.  The two streams touch disjoint columns of A.
+    // (Measured at n = 16384: 58.6 ms per inversion without look-ahead, 49.6 with; the rest
+    // update in 16 column chunks, chunk i released with panel i as a persistent GEMM capped at
+    // 132 CTAs: 50.9; capped persistent GEMMs of 64 / 100 / 132 CTAs for the whole rest: 57.)
     const bool ahead = w.side != nullptr && n >= 4 * GJE_NB && !env_flag("LYAP_GJE_NO_LOOKAHEAD");
     cudaStream_t P = ahead ? w.side : s;
     if (ahead) {
@@ -722,7 +736,8 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
             {
                 KTimer kt(KC_GJE_PANEL, P, (double)(n - k) * BW * BW + 2.0 * n * BW * BW,
                           (double)sizeof(T) * ((double)n * BW + (double)n * BW));
-                if (nt == 256 && rpt == 1) LYAP_TRY(panel_launch<T, 256, 1, false>(P, n, k, K0, nbk, A, w));
+                if (nt == 128) LYAP_TRY(panel_launch<T, 128, 2, false>(P, n, k, K0, nbk, A, w));
+                else if (nt == 256 && rpt == 1) LYAP_TRY(panel_launch<T, 256, 1, false>(P, n, k, K0, nbk, A, w));
                 else if (nt == 256) LYAP_TRY(panel_launch<T, 256, 2, false>(P, n, k, K0, nbk, A, w));
                 else if (nt == 512 && rpt == 1 && !xout) LYAP_TRY(panel_launch<T, 512, 1, false>(P, n, k, K0, nbk, A, w));
                 else if (nt == 512 && rpt == 1) LYAP_TRY(panel_launch<T, 512, 1, true>(P, n, k, K0, nbk, A, w));
