@@ -204,6 +204,9 @@ gje_ip_panel_kernel(int n, int k, int K0, int nbk, T *__restrict__ A, T *__restr
 #define IPPROF() do { } while (0)
 #endif
     IPPROF();
+    // programmatic dependent launch: the next kernel of the stream may set up beside this one
+    // (it waits for this grid's completion before it reads or writes anything)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (tid == 0) {
         ptx::mbar_init(&mbar[0], 1);
         ptx::mbar_init(&mbar[1], 1);
@@ -212,6 +215,8 @@ gje_ip_panel_kernel(int n, int k, int K0, int nbk, T *__restrict__ A, T *__restr
         ptx::mbar_arrive_expect_tx(&mbar[2], 32 * 32 * 4);       // 32 rows of L11, 128 bytes each
         sflag = 0;
     }
+    // (programmatic dependent launch: barrier setup above overlaps the previous kernel's tail)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // rows: thread tid of CTA q owns physical rows q RB + RPT tid + h
     float row[RPT][BW];
     int pos[RPT];
@@ -585,6 +590,8 @@ gje_ip_x_kernel(int n, int k, T *__restrict__ A, const int *__restrict__ pos_g, 
 {
     constexpr int VE = Ld16<T>::E;
     __shared__ __align__(16) float TL[2][32 * 32];               // T, Linv
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int e = threadIdx.x; e < 2 * 32 * 32; e += blockDim.x) TL[e >> 10][e & 1023] = Tg[e];
     __syncthreads();
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
@@ -704,12 +711,13 @@ __global__ void iota2_kernel(int n, int *a, int *b) {
 }
 
 template <typename T>
-int ip_gemm(cudaStream_t s, int M, int N, int K, const T *A, long lda, const T *B, long ldb, T *C, long ldc, int cap = 0)
+int ip_gemm(cudaStream_t s, int M, int N, int K, const T *A, long lda, const T *B, long ldb, T *C, long ldc, int cap = 0,
+            bool pdl = false)
 {
     if constexpr (std::is_same<T, float>::value)
         return gemm_strided<float, float, float, float>(s, M, N, K, 1.0f, A, lda, 1, B, 1, ldb, 1.0f, C, ldc, 1);
     else
-        return tc_gemm(s, Prec<T>::code, M, N, K, 1.0f, A, lda, B, ldb, 1.0f, C, ldc, 0, cap);
+        return tc_gemm(s, Prec<T>::code, M, N, K, 1.0f, A, lda, B, ldb, 1.0f, C, ldc, 0, cap, pdl);
 }
 
 template <typename T, int NT, int RPT, bool XOUT>
@@ -729,19 +737,28 @@ int panel_launch(cudaStream_t s, int n, int k, int K0, int nbk, T *A, GjeWork &w
     cfg.blockDim = dim3(NT, 1, 1);
     cfg.dynamicSmemBytes = dsm;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    // programmatic dependent launch of the step's three kernels: 3 % at n <= 4096; above, the
+    // early-resident CTAs of the next kernel take SMs from the look-ahead update (n = 16384:
+    // 60.8 against 46.4 ms per inversion), so it is off there
+    const bool pdl = n <= 4096 && !env_flag("LYAP_GJE_NO_PDL");
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = nc;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 2 : 1;
     LYAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, n, k, K0, nbk, A, (T *)w.X, (T *)w.B, w.invperm, w.rowperm, w.ipiv,
                                      w.info, w.ldet, (float *)w.Pglob, (float *)w.Tg));
     LYAP_TRY(launched());
     if (XOUT) {
-        gje_ip_x_kernel<T><<<std::min(ceil_div(n, 128), 592), 128, 0, s>>>(n, k, A, w.invperm, (const float *)w.Pglob,
-                                                                          (const float *)w.Tg, (T *)w.X);
+        cudaLaunchConfig_t cx = {};
+        cx.gridDim = dim3(std::min(ceil_div(n, 128), 592)); cx.blockDim = dim3(128); cx.stream = s;
+        cx.attrs = at + 1; cx.numAttrs = pdl ? 1 : 0;
+        LYAP_CUDA_TRY(cudaLaunchKernelEx(&cx, gje_ip_x_kernel<T>, n, k, A, (const int *)w.invperm, (const float *)w.Pglob,
+                                         (const float *)w.Tg, (T *)w.X));
         LYAP_TRY(launched());
     }
     return LYAP_OK;
@@ -791,7 +808,8 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
                 else LYAP_TRY(panel_launch<T, 1024, 1, true>(P, n, k, K0, nbk, A, w));
             }
             KTimer kt(KC_GJE_UPDATE, P);
-            LYAP_TRY(ip_gemm<T>(P, n, nbk, BW, (const T *)w.X, BW, (const T *)w.B + (size_t)K0 * BW, BW, A + K0, n));
+            const bool pdl = n <= 4096 && !env_flag("LYAP_GJE_NO_PDL");
+            LYAP_TRY(ip_gemm<T>(P, n, nbk, BW, (const T *)w.X, BW, (const T *)w.B + (size_t)K0 * BW, BW, A + K0, n, 0, pdl));
         }
         if (ahead) {
             LYAP_CUDA_TRY(cudaEventRecord(w.ev_b, P));             // inner steps of this block done

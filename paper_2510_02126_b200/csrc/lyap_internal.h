@@ -32,9 +32,10 @@ inline bool use_simt_gemm() {
     return v == 1;
 }
 // tcgen05 GEMM (tc_gemm.cu): C = alpha A B^T + beta C, 16-bit A (M x K), B (N x K) row-major
-// max_ctas > 0 caps the persistent kernel's grid (SMs left free for concurrent work)
+// max_ctas > 0 caps the persistent kernel's grid (SMs left free for concurrent work), < 0: one CTA per
+// tile; pdl: programmatic dependent launch (the kernel's setup overlaps the previous kernel's tail)
 int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const void *A, long lda, const void *B,
-            long ldb, float beta, void *C, long ldc, int colmajor, int max_ctas = 0);
+            long ldb, float beta, void *C, long ldc, int colmajor, int max_ctas = 0, bool pdl = false);
 int col_gather(cudaStream_t s, int n, int prec, const void *G, const int *invperm, void *out);
 template <typename T> int gemm_update(cudaStream_t s, int n, int b, const T *X, const T *B, T *A);
 

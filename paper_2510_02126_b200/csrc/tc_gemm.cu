@@ -130,6 +130,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
+    // programmatic dependent launch: the setup above overlaps the previous kernel's tail;
+    // every thread waits here before touching its inputs / outputs (a no-op otherwise)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer (the C tile first when it is blended in)
@@ -281,6 +284,8 @@ tc_gemm_persistent_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_
     const int tiles_n = (N + BN - 1) / BN, tiles = tiles_n * ((M + BM - 1) / BM);
     const int nk = (K + BK - 1) / BK;
     const bool blend = (beta != 0.f);
+    // one wave of CTAs: the next kernel of the stream may set up beside this one (PDL)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x == 0) {
         for (int i = 0; i < PSTAGES; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
         for (int i = 0; i < 2; i++) {
@@ -303,6 +308,9 @@ tc_gemm_persistent_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tmem_slot;
+    // programmatic dependent launch: the setup above overlaps the previous kernel's tail;
+    // every thread waits here before touching its inputs / outputs (a no-op otherwise)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == 0) {
         if (lane == 0) {
@@ -443,8 +451,23 @@ int make_map(CUtensorMap *m, const void *ptr, int prec, long rows, long cols, lo
 }  // namespace
 
 // C = alpha * A (M x K, ld lda) * B^T (B: N x K, ld ldb) + beta * C  (C ld ldc, row- or column-major)
+namespace {
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid; cfg.blockDim = block; cfg.dynamicSmemBytes = smem; cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at; cfg.numAttrs = pdl ? 1 : 0;
+    LYAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, KArgs(args)...));
+    return LYAP_OK;
+}
+}  // namespace
+
 int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const void *A, long lda, const void *B,
-            long ldb, float beta, void *C, long ldc, int colmajor, int max_ctas)
+            long ldb, float beta, void *C, long ldc, int colmajor, int max_ctas, bool pdl)
 {
     if (M <= 0 || N <= 0 || K <= 0) return LYAP_OK;
     if (prec != LYAP_BF16 && prec != LYAP_FP16) return LYAP_ERR_ARG;
@@ -479,9 +502,11 @@ int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const vo
     if (ctma && tiles >= nsm && max_ctas >= 0 && !env_flag("LYAP_TC_NONPERSISTENT")) {
         const int g = std::min(tiles, max_ctas > 0 ? std::min(max_ctas, nsm) : nsm);
         if (prec == LYAP_BF16)
-            tc_gemm_persistent_kernel<__nv_bfloat16><<<g, tc::PTHREADS, tc::PSMEM, s>>>(ma, mb, mc, M, N, K, alpha, beta);
+            LYAP_TRY(launch_pdl(tc_gemm_persistent_kernel<__nv_bfloat16>, dim3(g), dim3(tc::PTHREADS), tc::PSMEM, s, pdl, ma, mb, mc,
+                                M, N, K, alpha, beta));
         else
-            tc_gemm_persistent_kernel<__half><<<g, tc::PTHREADS, tc::PSMEM, s>>>(ma, mb, mc, M, N, K, alpha, beta);
+            LYAP_TRY(launch_pdl(tc_gemm_persistent_kernel<__half>, dim3(g), dim3(tc::PTHREADS), tc::PSMEM, s, pdl, ma, mb, mc, M, N,
+                                K, alpha, beta));
         return launched();
     }
     if (prec == LYAP_BF16)
