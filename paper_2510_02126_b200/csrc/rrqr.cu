@@ -392,7 +392,11 @@ struct Rrqr3Args {
     double *pw;         // gridDim x (RQ_NB + 1): slice partials of V^T u and ||u||^2
 };
 
-__global__ void __launch_bounds__(256, 2)
+// NT = 256 with two CTAs per SM while the pivot column (c doubles of shared memory per CTA)
+// allows it; above ~13 K rows only one CTA fits, and 512 threads keep 16 warps of loads in
+// flight per SM (the per-step GEMV is HBM bound: configs[3] with the fp32 solver, c ~ 12000).
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
 rrqr3_kernel(Rrqr3Args a)
 {
     cg::grid_group grid = cg::this_grid();
@@ -400,8 +404,8 @@ rrqr3_kernel(Rrqr3Args a)
     double *ush = rq_sm;                     // c: updated pivot column -> reflector v (rows j..)
     __shared__ double wv[RQ_NB];             // V[j:, 0:jj]^T v
     __shared__ double red[32];
-    __shared__ double s_best[8], s_sum[8];
-    __shared__ int s_idx[8], s_flag[8];
+    __shared__ double s_best[NT / 32], s_sum[NT / 32];
+    __shared__ int s_idx[NT / 32], s_flag[NT / 32];
     __shared__ double s_t;
     __shared__ int s_bi, s_fl;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
@@ -557,9 +561,21 @@ rrqr3_kernel(Rrqr3Args a)
             if (col == pc) { if (lane == t) m_act = false; continue; }
             if (!__shfl_sync(0xffffffffu, (int)m_act, t)) continue;
             const double *y = a.M + (long)col * c;
+            // four partial sums: the fp64 multiply-add chain of 16 in-flight loads would
+            // otherwise serialise behind the loads of the next 16
             double d = 0.0;
-#pragma unroll 16
-            for (int i = j + lane; i < c; i += 32) d = fma(y[i], ush[i], d);
+            {
+                double d1 = 0.0, d2 = 0.0, d3 = 0.0;
+                int i = j + lane;
+                for (; i + 96 < c; i += 128) {
+                    d = fma(y[i], ush[i], d);
+                    d1 = fma(y[i + 32], ush[i + 32], d1);
+                    d2 = fma(y[i + 64], ush[i + 64], d2);
+                    d3 = fma(y[i + 96], ush[i + 96], d3);
+                }
+                for (; i < c; i += 32) d = fma(y[i], ush[i], d);
+                d = (d + d1) + (d2 + d3);
+            }
             double *Fc = a.F + (long)col * RQ_NB;
             const double fl = (lane < jj) ? Fc[lane] : 0.0;
             const double corr = warp_sum(fl * wl);
@@ -669,15 +685,18 @@ static int rank_trunc_chol_blocked(cudaStream_t s, int n, int c, double tol, int
         int dev = 0, nsm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(rrqr3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(rrqr3_kernel<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(rrqr3_kernel<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         return Cfg{nsm, 0};
     }();
     const size_t smem = sizeof(double) * (size_t)c;
     if (smem > 200 * 1024) return LYAP_ERR_CAPACITY;
     int per = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr3_kernel, 256, smem);
-    const int grid = std::max(1, std::min(std::min(cfg.nsm * std::min(per, 2), w.p3_ctas), ceil_div(n, 8)));
-    if (n > 32 * 8 * grid) return LYAP_ERR_CAPACITY;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rrqr3_kernel<256, 2>, 256, smem);
+    const bool wide = per < 2 && !env_flag("LYAP_RRQR_256");     // one CTA per SM: 512 threads
+    const int nth = wide ? 512 : 256;
+    const int grid = std::max(1, std::min(std::min(cfg.nsm * (wide ? 1 : std::min(per, 2)), w.p3_ctas), ceil_div(n, nth / 32)));
+    if (n > 32 * (nth / 32) * grid) return LYAP_ERR_CAPACITY;
     fill_int_kernel<<<std::min(ceil_div(n, 256), 1024), 256, 0, s>>>(n, 1, w.act3);
     LYAP_TRY(launched());
     const int kmax = c < n ? c : n;
@@ -690,7 +709,8 @@ static int rank_trunc_chol_blocked(cudaStream_t s, int n, int c, double tol, int
                     (int *)(w.p3 + 4 * w.p3_ctas), (int *)(w.p3 + 4 * w.p3_ctas) + 2 * w.p3_ctas,
                     w.ints, w.act3, w.st3, ist, w.ug3, w.pw3};
         void *args[] = {&a};
-        LYAP_CUDA_TRY(cudaLaunchCooperativeKernel((void *)rrqr3_kernel, dim3(grid), dim3(256), args, smem, s));
+        LYAP_CUDA_TRY(cudaLaunchCooperativeKernel(wide ? (void *)rrqr3_kernel<512, 1> : (void *)rrqr3_kernel<256, 2>, dim3(grid),
+                                                  dim3(nth), args, smem, s));
         LYAP_TRY(launched());
         LYAP_CUDA_TRY(cudaMemcpyAsync(hs, ist, sizeof(int) * 3, cudaMemcpyDeviceToHost, s));
         LYAP_CUDA_TRY(cudaStreamSynchronize(s));

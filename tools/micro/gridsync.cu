@@ -22,6 +22,22 @@ __global__ void k2(int iters, unsigned *bar, int *x) {
         __syncthreads();
     }
 }
+// flag-array barrier: every CTA publishes its own sequence number (one release store, no
+// atomic), warp 0 of every CTA polls all flags (acquire loads), one __syncthreads each side
+__global__ void k3(int iters, unsigned *flags) {
+    const unsigned nb = gridDim.x;
+    for (int i = 0; i < iters; i++) {
+        __syncthreads();
+        if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(flags + blockIdx.x * 32), "r"(i + 1) : "memory");
+        if (threadIdx.x < 32) {
+            for (unsigned b = threadIdx.x; b < nb; b += 32) {
+                unsigned v;
+                do { asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + b * 32) : "memory"); } while (v < (unsigned)(i + 1));
+            }
+        }
+        __syncthreads();
+    }
+}
 int main() {
     int *x; unsigned *bar; cudaMalloc(&x, 4); cudaMalloc(&bar, 4);
     int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
@@ -40,6 +56,12 @@ int main() {
         cudaLaunchCooperativeKernel((void*)k2, grid, 256, args2, 0, 0);
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms2; cudaEventElapsedTime(&ms2, a, b);
-        printf("grid %d: cg grid.sync %.3f us, custom barrier %.3f us (err %s)\n", grid, ms * 1e3 / iters, ms2 * 1e3 / iters, cudaGetErrorString(cudaGetLastError()));
+        unsigned *fl; cudaMalloc(&fl, 4 * 32 * 256); cudaMemset(fl, 0, 4 * 32 * 256);
+        void *args3[] = {&iters, &fl};
+        cudaEventRecord(a);
+        cudaLaunchCooperativeKernel((void*)k3, grid, 256, args3, 0, 0);
+        cudaEventRecord(b); cudaEventSynchronize(b);
+        float ms3; cudaEventElapsedTime(&ms3, a, b);
+        printf("grid %d: cg grid.sync %.3f us, custom barrier %.3f us, flag array %.3f us (err %s)\n", grid, ms * 1e3 / iters, ms2 * 1e3 / iters, ms3 * 1e3 / iters, cudaGetErrorString(cudaGetLastError()));
     }
 }
