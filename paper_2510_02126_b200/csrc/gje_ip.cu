@@ -215,6 +215,10 @@ gje_ip_panel_kernel(int n, int k, int K0, int nbk, T *__restrict__ A, T *__restr
         ptx::mbar_arrive_expect_tx(&mbar[2], 32 * 32 * 4);       // 32 rows of L11, 128 bytes each
         sflag = 0;
     }
+    // the cluster barrier that publishes the mbarrier initialisation is split: arrive here, wait
+    // after the row loads (their latency hides it)
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     // (programmatic dependent launch: barrier setup above overlaps the previous kernel's tail)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // rows: thread tid of CTA q owns physical rows q RB + RPT tid + h
@@ -243,7 +247,7 @@ gje_ip_panel_kernel(int n, int k, int K0, int nbk, T *__restrict__ A, T *__restr
         }
     }
     IPPROF();
-    cluster_sync_all();                                          // barriers initialised cluster-wide
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // barriers initialised cluster-wide
     IPPROF();
 
     // loop-invariant shared addresses (buffer 0; buffer 1 at a constant offset)

@@ -56,14 +56,22 @@ def _cases(G):
     M = (torch.randn(1024, 1024, device="cuda", generator=g) / 32 - 2 * torch.eye(1024, device="cuda")).to(torch.bfloat16)
     Z = torch.randn(200, 700, dtype=torch.float64, device="cuda", generator=g)
 
+    M2 = (torch.randn(2048, 2048, device="cuda", generator=g) / 45 - 2 * torch.eye(2048, device="cuda")).to(torch.float16)
+
     def inv():
         X = M.clone()
+        G.invert(X)
+        return X.float().flatten()
+
+    def inv2():          # n = 2048: implicit pivoting with the look-ahead stream and dependent launches
+        X = M2.clone()
         G.invert(X)
         return X.float().flatten()
     return {
         "syev": lambda: torch.cat([t.flatten() for t in G.syev(B)]),
         "qr": lambda: torch.cat([t.flatten() for t in G.qr(Aq)]),
         "invert": inv,
+        "invert_lookahead": inv2,
         "rank_trunc_chol": lambda: G.rank_trunc_chol(Z, 2 ** -6, "fp64").flatten(),
     }
 
