@@ -56,9 +56,6 @@ __device__ __forceinline__ void st_async_v4(uint32_t dst, const float4 &v, uint3
                  :: "r"(dst), "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
                     "r"(__float_as_uint(v.w)), "r"(mbar) : "memory");
 }
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 
 // (key, npos) lexicographic maximum over the lanes with `in`; returns the winning lane
 // (keys: 0 = no candidate; npos = ~position, so the lowest position wins ties)
@@ -271,7 +268,11 @@ gje_ip_panel_kernel(int n, int k, int K0, int nbk, T *__restrict__ A, T *__restr
     // a __syncthreads costs ~5 cycles on the SM, nine STS.128 per warp 400-1300 cycles per
     // column.  With 8 warps the early staging is cheaper than the longer chain (measured: 1690 vs
     // 1960 cycles per column at n = 1024; 2430 vs 2350 at n = 16384 with 16 warps x 2 rows).
+#ifdef LYAP_IP_LATE_ALL
+    constexpr bool LATE = true;
+#else
     constexpr bool LATE = NT >= 512;
+#endif
     // LATE: lane -> (destination CTA, 16-byte chunk) tasks of the winning warp
     constexpr int NTASK = (16 * (SLOTW / 4) + 31) / 32;          // 144 tasks at 16 CTAs: 5 per lane
     uint32_t t_inbox[LATE ? NTASK : 1], t_mbar[LATE ? NTASK : 1], t_chunk[LATE ? NTASK : 1];
@@ -305,6 +306,11 @@ gje_ip_panel_kernel(int n, int k, int K0, int nbk, T *__restrict__ A, T *__restr
             if (kk > key || (kk == key && pp > npos)) { key = kk; npos = pp; hsel = h; }
         }
         if constexpr (LATE) {
+            // every thread's reciprocal before the barrier (beside the reductions), so the
+            // division is not on the chain after it
+            float rinv_h[RPT];
+#pragma unroll
+            for (int h = 0; h < RPT; h++) rinv_h[h] = (row[h][0] != 0.f) ? 1.f / row[h][0] : 0.f;
             const int wl = warp_pick(key, npos);                 // the warp's best lane
             const uint32_t sa = a_myslot + buf * SLOT_B;
             if (lane == wl) sts128(sa + BW * 4, __uint_as_float(key), __uint_as_float(npos), 0.f, 0.f);
@@ -317,10 +323,9 @@ gje_ip_panel_kernel(int n, int k, int K0, int nbk, T *__restrict__ A, T *__restr
 #pragma unroll
                     for (int h = 0; h < RPT; h++)
                         if (h == hsel) {
-                            const float rinv = (row[h][0] != 0.f) ? 1.f / row[h][0] : 0.f;
 #pragma unroll
                             for (int c = 0; c < BW; c += 4) sts128(sa + c * 4, row[h][c], row[h][c + 1], row[h][c + 2], row[h][c + 3]);
-                            sts128(sa + BW * 4, __uint_as_float(key), __uint_as_float(npos), __int_as_float(r0 + h), rinv);
+                            sts128(sa + BW * 4, __uint_as_float(key), __uint_as_float(npos), __int_as_float(r0 + h), rinv_h[h]);
                         }
                 }
                 __syncwarp();
