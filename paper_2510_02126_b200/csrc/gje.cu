@@ -944,8 +944,12 @@ static int outer_gemm(cudaStream_t s, int M, int N, int K, const T *A, long lda,
 {
     if constexpr (std::is_same<T, float>::value)
         return gemm_strided<float, float, float, float>(s, M, N, K, 1.0f, A, lda, 1, B, 1, ldb, 1.0f, C, ldc, 1);
-    else
+    else {
+        // the rank-32 steps as in gje_ip.cu (same kernel: the two sweeps stay bitwise equal)
+        if (K == 32 && lda == 32 && ldb == 32 && rank32_update_ok(Prec<T>::code, N, A, B, C, ldc))
+            return rank32_update(s, Prec<T>::code, M, N, A, B, C, ldc);
         return tc_gemm(s, Prec<T>::code, M, N, K, 1.0f, A, lda, B, ldb, 1.0f, C, ldc, 0, cap);
+    }
 }
 
 template <typename T>
@@ -1061,6 +1065,8 @@ int gemm_update(cudaStream_t s, int n, int b, const T *X, const T *B, T *A)
     using Acc = typename Prec<T>::acc;
     // B holds the pivot rows transposed (Bt, n x b row-major): A += X Bt^T
     if constexpr (std::is_same<T, __half>::value || std::is_same<T, __nv_bfloat16>::value) {
+        if (!use_simt_gemm() && b == 32 && rank32_update_ok(Prec<T>::code, n, X, B, A, n))
+            return rank32_update(s, Prec<T>::code, n, n, X, B, A, n);
         if (!use_simt_gemm() && b % 8 == 0)     // TMA rows must be 16-byte multiples
             return tc_gemm(s, Prec<T>::code, n, n, b, 1.0f, X, b, B, b, 1.0f, A, n, 0);
     }

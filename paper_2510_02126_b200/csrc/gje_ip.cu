@@ -653,14 +653,16 @@ gje_ip_x_kernel(int n, int k, T *__restrict__ A, const int *__restrict__ pos_g, 
 // along the rows, transposed through shared memory, 16-byte stores along y.
 template <typename T>
 __global__ void __launch_bounds__(256)
-gje_ip_outer_prep_kernel(int n, int K0, int nb, T *__restrict__ A, const int *__restrict__ piv, T *__restrict__ Bo)
+gje_ip_outer_prep_kernel(int n, int K0, int nb, int eb, int ee, T *__restrict__ A, const int *__restrict__ piv,
+                         T *__restrict__ Bo)
 {
     constexpr int VE = 16 / (int)sizeof(T);                       // elements per 16-byte vector
     constexpr int TC = 64, TR = 128;                              // tile: columns x pivot rows
     __shared__ T tile[TR][TC + VE];                               // row stride keeps 16-byte alignment
     __shared__ int prow[TR];
-    const int nrest = n - nb;
-    const int e0 = blockIdx.x * TC, y0 = blockIdx.y * TR;
+    // rest columns [eb, ee) (indices that skip the block), eb a multiple of 64
+    const int nrest = ee;
+    const int e0 = eb + blockIdx.x * TC, y0 = blockIdx.y * TR;
     for (int y = threadIdx.x; y < TR; y += blockDim.x) prow[y] = (y0 + y < nb) ? piv[K0 + y0 + y] : -1;
     __syncthreads();
     // rest column e -> matrix column c (the block columns are skipped); K0 and nb are
@@ -725,8 +727,11 @@ int ip_gemm(cudaStream_t s, int M, int N, int K, const T *A, long lda, const T *
 {
     if constexpr (std::is_same<T, float>::value)
         return gemm_strided<float, float, float, float>(s, M, N, K, 1.0f, A, lda, 1, B, 1, ldb, 1.0f, C, ldc, 1);
-    else
+    else {
+        if (K == 32 && lda == 32 && ldb == 32 && rank32_update_ok(Prec<T>::code, N, A, B, C, ldc))
+            return rank32_update(s, Prec<T>::code, M, N, A, B, C, ldc, pdl);
         return tc_gemm(s, Prec<T>::code, M, N, K, 1.0f, A, lda, B, ldb, 1.0f, C, ldc, 0, cap, pdl);
+    }
 }
 
 template <typename T, int NT, int RPT, bool XOUT>
@@ -825,15 +830,27 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
             LYAP_CUDA_TRY(cudaStreamWaitEvent(s, w.ev_b, 0));
         }
         if (n - nbk > 0) {
-            gje_ip_outer_prep_kernel<T><<<dim3(ceil_div(n - nbk, 64), ceil_div(nbk, 128)), 256, 0, s>>>(n, K0, nbk, A, w.rowperm, (T *)w.Bo);
-            LYAP_TRY(launched());
+            // B_outer in rest-column indices e (e < K0: column e, else column e + nbk)
+            auto prep = [&](int eb, int ee) -> int {
+                if (ee <= eb) return LYAP_OK;
+                gje_ip_outer_prep_kernel<T><<<dim3(ceil_div(ee - eb, 64), ceil_div(nbk, 128)), 256, 0, s>>>(
+                    n, K0, nbk, eb, ee, A, w.rowperm, (T *)w.Bo);
+                return launched();
+            };
             KTimer kt(KC_GJE_UPDATE, s);
             const int cr = K0 + nbk;
             const int cn = ahead ? std::min(n, cr + GJE_NB) : cr;
             if (ahead && cn > cr) {
+                // the next block's columns first (B_outer for them, their update), then P may start;
+                // the other columns' B_outer and update run beside P
+                LYAP_TRY(prep(K0, K0 + (cn - cr)));
                 LYAP_TRY(ip_gemm<T>(s, n, cn - cr, nbk, A + K0, n, (const T *)w.Bo + (size_t)cr * nbk, nbk, A + cr, n));
                 LYAP_CUDA_TRY(cudaEventRecord(w.ev_a, s));
                 LYAP_CUDA_TRY(cudaStreamWaitEvent(P, w.ev_a, 0));
+                LYAP_TRY(prep(0, K0));
+                LYAP_TRY(prep(K0 + (cn - cr), n - nbk));
+            } else {
+                LYAP_TRY(prep(0, n - nbk));
             }
             int cap = (ahead && cn > cr) ? -1 : 0;
             if (const char *e = getenv("LYAP_GJE_LA_CAP")) cap = (ahead && cn > cr) ? atoi(e) : 0;   // tuning

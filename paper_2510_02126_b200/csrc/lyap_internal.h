@@ -36,6 +36,10 @@ inline bool use_simt_gemm() {
 // tile; pdl: programmatic dependent launch (the kernel's setup overlaps the previous kernel's tail)
 int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const void *A, long lda, const void *B,
             long ldb, float beta, void *C, long ldc, int colmajor, int max_ctas = 0, bool pdl = false);
+// rank-32 update C (M x N, ld ldc) += X (M x 32) Bt^T (Bt: N x 32), 16-bit storage (rank_update.cu)
+bool rank32_update_ok(int prec, int N, const void *X, const void *Bt, const void *C, long ldc);
+int rank32_update(cudaStream_t s, int prec, int M, int N, const void *X, const void *Bt, void *C, long ldc,
+                  bool pdl = false);
 int col_gather(cudaStream_t s, int n, int prec, const void *G, const int *invperm, void *out);
 template <typename T> int gemm_update(cudaStream_t s, int n, int b, const T *X, const T *B, T *A);
 
