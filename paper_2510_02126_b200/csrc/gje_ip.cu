@@ -501,18 +501,24 @@ gje_ip_panel_kernel(int n, int k, int K0, int nbk, T *__restrict__ A, T *__restr
 
     IPPROF();
     if constexpr (XOUT) {
-        // ---- export: active rows' multipliers, positions, T and Linv (gje_ip_x_kernel forms X)
+        // ---- export: multipliers (active rows), panel entries (finished rows), positions, T and
+        // Linv: the X rows are formed by the fused update kernel (or gje_ip_x_kernel)
 #pragma unroll
         for (int h = 0; h < RPT; h++) {
             const int r = r0 + h;
             if (r >= n) continue;
             const int p = pos[h];
             pos_g[r] = p;
+            float4 *dst = reinterpret_cast<float4 *>(Pg + (long)r * BW);
             if (p >= k + BW) {
-                float4 *dst = reinterpret_cast<float4 *>(Pg + (long)r * BW);
                 const float *lc = &Lsm[h * NT + tid];
 #pragma unroll
                 for (int c = 0; c < BW; c += 4) dst[c / 4] = make_float4(lc[c * LS], lc[(c + 1) * LS], lc[(c + 2) * LS], lc[(c + 3) * LS]);
+            } else if (p < k) {
+                // finished rows: their panel entries (never shifted), for the fused X + update kernel
+                // (several of its CTAs read a row's entries while another overwrites them in A)
+#pragma unroll
+                for (int c = 0; c < BW; c += 4) dst[c / 4] = make_float4(row[h][c], row[h][c + 1], row[h][c + 2], row[h][c + 3]);
             }
         }
         if (q == 0)
@@ -735,7 +741,7 @@ int ip_gemm(cudaStream_t s, int M, int N, int K, const T *A, long lda, const T *
 }
 
 template <typename T, int NT, int RPT, bool XOUT>
-int panel_launch(cudaStream_t s, int n, int k, int K0, int nbk, T *A, GjeWork &w)
+int panel_launch(cudaStream_t s, int n, int k, int K0, int nbk, T *A, GjeWork &w, bool xkernel)
 {
     auto kern = gje_ip_panel_kernel<T, NT, RPT, XOUT>;
     constexpr int dsm = 32 * (NT * RPT + 1) * (int)sizeof(float);     // Lsm
@@ -767,7 +773,7 @@ int panel_launch(cudaStream_t s, int n, int k, int K0, int nbk, T *A, GjeWork &w
     LYAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, n, k, K0, nbk, A, (T *)w.X, (T *)w.B, w.invperm, w.rowperm, w.ipiv,
                                      w.info, w.ldet, (float *)w.Pglob, (float *)w.Tg));
     LYAP_TRY(launched());
-    if (XOUT) {
+    if (XOUT && xkernel) {
         cudaLaunchConfig_t cx = {};
         cx.gridDim = dim3(std::min(ceil_div(n, 128), 592)); cx.blockDim = dim3(128); cx.stream = s;
         cx.attrs = at + 1; cx.numAttrs = pdl ? 1 : 0;
@@ -793,6 +799,13 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
     if (nt == 128) rpt = 2;
     if (ceil_div(n, nt * rpt) > 16) { nt = n <= 8192 ? 512 : 1024; rpt = 1; }
     const bool xout = !env_flag("LYAP_GJE_IP_XIN");             // 512-thread panels: X rows by the separate kernel
+    // 16-bit storage: the X rows are formed inside the rank-32 update kernel (rank_update.cu)
+    constexpr bool half_t = !std::is_same<T, float>::value;
+    // (measured: n = 1024 1.42 -> 1.35 ms per inversion, 8192 18.8 -> 17.7, 16384 45.4 -> 43.9; at
+    // n = 4096 the X phase on the panel's 16 SMs is as fast, 6.24 vs 6.35 ms: in-panel there)
+    const bool fused = half_t && n % 8 == 0 && !(n > 2048 && n <= 4096) && !env_flag("LYAP_GJE_NO_FUSEX") &&
+                       !env_flag("LYAP_NO_RANK32");
+    const bool xk = !fused;
     // Look-ahead: the panels and rank-32 updates of block K0 + NB run on the high-priority
     // stream P while the main stream applies the rest of block K0's rank-NB update.  Order on
     // the main stream: B_outer, the update of the NEXT block's columns (then P may start), the
@@ -813,17 +826,23 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
             {
                 KTimer kt(KC_GJE_PANEL, P, (double)(n - k) * BW * BW + 2.0 * n * BW * BW,
                           (double)sizeof(T) * ((double)n * BW + (double)n * BW));
-                if (nt == 128) LYAP_TRY(panel_launch<T, 128, 2, false>(P, n, k, K0, nbk, A, w));
-                else if (nt == 256 && rpt == 1) LYAP_TRY(panel_launch<T, 256, 1, false>(P, n, k, K0, nbk, A, w));
-                else if (nt == 256) LYAP_TRY(panel_launch<T, 256, 2, false>(P, n, k, K0, nbk, A, w));
-                else if (nt == 512 && rpt == 1 && !xout) LYAP_TRY(panel_launch<T, 512, 1, false>(P, n, k, K0, nbk, A, w));
-                else if (nt == 512 && rpt == 1) LYAP_TRY(panel_launch<T, 512, 1, true>(P, n, k, K0, nbk, A, w));
-                else if (nt == 512) LYAP_TRY(panel_launch<T, 512, 2, true>(P, n, k, K0, nbk, A, w));
-                else LYAP_TRY(panel_launch<T, 1024, 1, true>(P, n, k, K0, nbk, A, w));
+                if (nt == 128) LYAP_TRY(panel_launch<T, 128, 2, false>(P, n, k, K0, nbk, A, w, xk));
+                else if (nt == 256 && rpt == 1 && fused) LYAP_TRY(panel_launch<T, 256, 1, true>(P, n, k, K0, nbk, A, w, xk));
+                else if (nt == 256 && rpt == 1) LYAP_TRY(panel_launch<T, 256, 1, false>(P, n, k, K0, nbk, A, w, xk));
+                else if (nt == 256) LYAP_TRY(panel_launch<T, 256, 2, false>(P, n, k, K0, nbk, A, w, xk));
+                else if (nt == 512 && rpt == 1 && !xout) LYAP_TRY(panel_launch<T, 512, 1, false>(P, n, k, K0, nbk, A, w, xk));
+                else if (nt == 512 && rpt == 1) LYAP_TRY(panel_launch<T, 512, 1, true>(P, n, k, K0, nbk, A, w, xk));
+                else if (nt == 512) LYAP_TRY(panel_launch<T, 512, 2, true>(P, n, k, K0, nbk, A, w, xk));
+                else LYAP_TRY(panel_launch<T, 1024, 1, true>(P, n, k, K0, nbk, A, w, xk));
             }
             KTimer kt(KC_GJE_UPDATE, P);
             const bool pdl = n <= 4096 && !env_flag("LYAP_GJE_NO_PDL");
-            LYAP_TRY(ip_gemm<T>(P, n, nbk, BW, (const T *)w.X, BW, (const T *)w.B + (size_t)K0 * BW, BW, A + K0, n, 0, pdl));
+            const bool xexp = !(nt == 128 || (nt == 256 && rpt == 2) || (nt == 512 && rpt == 1 && !xout));   // panel exported
+            if (fused && xexp)
+                LYAP_TRY(rank32_fused_update(P, Prec<T>::code, n, nbk, k, K0, (const float *)w.Pglob, (const float *)w.Tg,
+                                             w.invperm, (const T *)w.B + (size_t)K0 * BW, A + K0, n, pdl));
+            else
+                LYAP_TRY(ip_gemm<T>(P, n, nbk, BW, (const T *)w.X, BW, (const T *)w.B + (size_t)K0 * BW, BW, A + K0, n, 0, pdl));
         }
         if (ahead) {
             LYAP_CUDA_TRY(cudaEventRecord(w.ev_b, P));             // inner steps of this block done

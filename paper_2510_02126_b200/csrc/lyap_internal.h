@@ -40,6 +40,9 @@ int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const vo
 bool rank32_update_ok(int prec, int N, const void *X, const void *Bt, const void *C, long ldc);
 int rank32_update(cudaStream_t s, int prec, int M, int N, const void *X, const void *Bt, void *C, long ldc,
                   bool pdl = false);
+// the same with the X tile formed in the kernel from the panel's export (see rank_update.cu)
+int rank32_fused_update(cudaStream_t s, int prec, int M, int N, int k, int K0, const float *P, const float *TL,
+                        const int *pos, const void *Bt, void *C, long ldc, bool pdl = false);
 int col_gather(cudaStream_t s, int n, int prec, const void *G, const int *invperm, void *out);
 template <typename T> int gemm_update(cudaStream_t s, int n, int b, const T *X, const T *B, T *A);
 
