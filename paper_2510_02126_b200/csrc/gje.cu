@@ -775,7 +775,7 @@ int GjeWork::alloc(int n_, int prec_) {
     LYAP_CUDA_TRY(cudaMalloc(&Pglob, acc * (size_t)n * b));
     LYAP_CUDA_TRY(cudaMalloc(&Tg, acc * 2 * 32 * 32));   // T, then Linv
     if ((prec == LYAP_FP16 || prec == LYAP_BF16 || prec == LYAP_FP32) && n % 8 == 0 && n >= 2 * GJE_NB) {
-        LYAP_CUDA_TRY(cudaMalloc(&Bo, es * (size_t)n * GJE_NB));
+        LYAP_CUDA_TRY(cudaMalloc(&Bo, es * (size_t)n * GJE_NB_MAX));
         LYAP_CUDA_TRY(cudaMalloc(&tmp2, es * (size_t)n * 2 * GJE_NB));
         LYAP_CUDA_TRY(cudaMalloc(&oints, sizeof(int) * (5 * GJE_NB + 8 + (size_t)n)));
         int lo_p = 0, hi_p = 0;

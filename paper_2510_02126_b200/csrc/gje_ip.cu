@@ -798,6 +798,9 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
     if (const char *e = getenv("LYAP_GJE_IP_RPT")) rpt = atoi(e);
     if (nt == 128) rpt = 2;
     if (ceil_div(n, nt * rpt) > 16) { nt = n <= 8192 ? 512 : 1024; rpt = 1; }
+    // outer block: GJE_NB columns (w.Bo holds n x GJE_NB_MAX; LYAP_GJE_IP_NB for tuning)
+    int NB = GJE_NB;
+    if (const char *e = getenv("LYAP_GJE_IP_NB")) NB = std::max(64, std::min(GJE_NB_MAX, atoi(e) / 32 * 32));
     const bool xout = !env_flag("LYAP_GJE_IP_XIN");             // 512-thread panels: X rows by the separate kernel
     // 16-bit storage: the X rows are formed inside the rank-32 update kernel (rank_update.cu)
     constexpr bool half_t = !std::is_same<T, float>::value;
@@ -814,14 +817,14 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
     // (Measured at n = 16384: 58.6 ms per inversion without look-ahead, 49.6 with; the rest
     // update in 16 column chunks, chunk i released with panel i as a persistent GEMM capped at
     // 132 CTAs: 50.9; capped persistent GEMMs of 64 / 100 / 132 CTAs for the whole rest: 57.)
-    const bool ahead = w.side != nullptr && n >= 4 * GJE_NB && !env_flag("LYAP_GJE_NO_LOOKAHEAD");
+    const bool ahead = w.side != nullptr && n >= 4 * NB && !env_flag("LYAP_GJE_NO_LOOKAHEAD");
     cudaStream_t P = ahead ? w.side : s;
     if (ahead) {
         LYAP_CUDA_TRY(cudaEventRecord(w.ev_a, s));
         LYAP_CUDA_TRY(cudaStreamWaitEvent(P, w.ev_a, 0));
     }
-    for (int K0 = 0; K0 < n; K0 += GJE_NB) {
-        const int nbk = std::min(GJE_NB, n - K0);
+    for (int K0 = 0; K0 < n; K0 += NB) {
+        const int nbk = std::min(NB, n - K0);
         for (int k = K0; k < K0 + nbk; k += BW) {
             {
                 KTimer kt(KC_GJE_PANEL, P, (double)(n - k) * BW * BW + 2.0 * n * BW * BW,
@@ -858,7 +861,7 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
             };
             KTimer kt(KC_GJE_UPDATE, s);
             const int cr = K0 + nbk;
-            const int cn = ahead ? std::min(n, cr + GJE_NB) : cr;
+            const int cn = ahead ? std::min(n, cr + NB) : cr;
             if (ahead && cn > cr) {
                 // the next block's columns first (B_outer for them, their update), then P may start;
                 // the other columns' B_outer and update run beside P

@@ -6,7 +6,13 @@
 namespace lyap {
 
 // Workspace of the blocked Gauss-Jordan inversion (gje.cu).
-constexpr int GJE_NB = 512;        // outer block of the two-level Gauss-Jordan scheme (16-bit types)
+// outer block of the two-level Gauss-Jordan scheme (16-bit types and fp32).  Measured with the
+// implicit-pivoting sweep (ms per fp16 inversion at n = 4096 / 8192 / 16384): 128 columns 6.37 /
+// 17.6 / 47.5, 192: 6.34 / 17.3 / 44.0, 256: 6.21 / 17.0 / 42.3, 384: 6.20 / 17.4 / 43.4, 512: 6.29 /
+// 17.7 / 43.9, 1024: 6.58 / 19.1 / 49.2 -- narrower blocks halve the rank-32 updates' traffic, and
+// the look-ahead hides the extra rank-NB updates
+constexpr int GJE_NB = 256;
+constexpr int GJE_NB_MAX = 1024;   // capacity of the outer-block workspace (tuning of gje_ip.cu's block)
 struct GjeWork {
     int n = 0, prec = 0;
     void *X = nullptr, *B = nullptr, *tmp = nullptr, *Pglob = nullptr, *Tg = nullptr, *Bo = nullptr, *tmp2 = nullptr;
