@@ -804,9 +804,10 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
     const bool xout = !env_flag("LYAP_GJE_IP_XIN");             // 512-thread panels: X rows by the separate kernel
     // 16-bit storage: the X rows are formed inside the rank-32 update kernel (rank_update.cu)
     constexpr bool half_t = !std::is_same<T, float>::value;
-    // (measured: n = 1024 1.42 -> 1.35 ms per inversion, 8192 18.8 -> 17.7, 16384 45.4 -> 43.9; at
-    // n = 4096 the X phase on the panel's 16 SMs is as fast, 6.24 vs 6.35 ms: in-panel there)
-    const bool fused = half_t && n % 8 == 0 && !(n > 2048 && n <= 4096) && !env_flag("LYAP_GJE_NO_FUSEX") &&
+    // (measured: n = 1024 1.43 -> 1.35 ms per inversion, 3072 4.50 -> 4.36, 8192 18.6 -> 17.0, 16384
+    // 45.4 -> 43.9; with the full 16-CTA cluster of 256-thread CTAs (n = 4096) the X phase on the
+    // panel's 16 SMs is as fast, 6.21 vs 6.25 ms: in-panel there)
+    const bool fused = half_t && n % 8 == 0 && !(n > 3584 && n <= 4096) && !env_flag("LYAP_GJE_NO_FUSEX") &&
                        !env_flag("LYAP_NO_RANK32");
     const bool xk = !fused;
     // Look-ahead: the panels and rank-32 updates of block K0 + NB run on the high-priority
