@@ -20,16 +20,19 @@
 //       row.  The pushed pivot row is row j of the block's LU factors, so every CTA
 //       collects L11/U11 as a by-product;
 //     * every CTA forms Linv, Uinv, T = U11^{-1} L11^{-1} (redundantly: no exchange);
-//     * every thread forms its row of the multiplier block X (finished rows -a T, pivot rows
-//       T, active rows -l Linv), writes it in u_s and zeroes its panel entries;
-//     * the cluster copies the 32 pivot rows' block columns into B (K-major for the GEMM,
+//     * every thread exports its row's multipliers (active rows) or panel entries (finished
+//       rows) in fp32, CTA 0 exports T and Linv;
+//     * the cluster copies the 32 pivot rows' block columns into B (K-major for the update,
 //       B[:, panel] = I) and zeroes them;
-//   then A[:, block] += X B on the tensor cores (tcgen05, K = 32).
-// After the 16 panels of an outer block of 512 columns, one kernel moves the 512 pivot
-// rows' remaining entries into B_outer and one GEMM applies the rank-512 update.  At the
-// end M_phys holds A^{-1}[pos[r], piv(c)] = M_phys[r, c]; a row-gathering copy writes
-// G[i, :] = M_phys[piv(i), :], the layout the Newton update and the Z-side consume
-// (A^{-1}[i][l] = G[i][invperm[l]], rowperm = piv, invperm = pos).
+//   then A[:, block] += X B with X = [-a T ; T ; -l Linv] formed tile by tile inside the
+//   rank-32 update kernel (rank_update.cu; fp32 storage: X in the panel or by gje_ip_x_kernel,
+//   update on the SIMT GEMM).
+// After the 8 panels of an outer block of 256 columns, one kernel moves the 256 pivot rows'
+// remaining entries into B_outer and the tensor cores (tcgen05) apply the rank-256 update; the
+// next block's panels run beside it on a second stream (look-ahead).  At the end M_phys holds
+// A^{-1}[pos[r], piv(c)] = M_phys[r, c]; a row-gathering copy writes G[i, :] = M_phys[piv(i), :],
+// the layout the Newton update and the Z-side consume (A^{-1}[i][l] = G[i][invperm[l]],
+// rowperm = piv, invperm = pos).
 #include <cooperative_groups.h>
 #include "common.cuh"
 #include "gemm_simt.cuh"
