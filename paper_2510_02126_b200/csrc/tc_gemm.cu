@@ -55,6 +55,22 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
         :: "r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
 }
+// the same with an L2 eviction policy (streaming C tiles of the look-ahead update must not push
+// the next block's columns, which the concurrent panels read, out of the L2)
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;"
+        :: "r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap *map, const void *src, int c0, int c1, uint64_t pol) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;"
+                 :: "l"(map), "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(b)) : "memory");
 }
@@ -96,7 +112,7 @@ template <typename T>
 __global__ void __launch_bounds__(128, 3)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, int M, int N, int K, float alpha, float beta,
-               T *__restrict__ C, long ldc, int colmajor, int ctma, int ns)
+               T *__restrict__ C, long ldc, int colmajor, int ctma, int ns, int cstream)
 {
     using namespace tc;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -140,7 +156,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             tc::mbar_expect_tx(cbar, C_STAGE);
             for (int w = 0; w < 4; w++)
                 for (int hh = 0; hh < 2; hh++)
-                    tc::tma_load_2d(sC + (w * 2 + hh) * 4096, &tmC, cbar, n0 + 64 * hh, m0 + 32 * w);
+                    if (cstream) tc::tma_load_2d_hint(sC + (w * 2 + hh) * 4096, &tmC, cbar, n0 + 64 * hh, m0 + 32 * w, tc::l2_evict_first());
+                    else tc::tma_load_2d(sC + (w * 2 + hh) * 4096, &tmC, cbar, n0 + 64 * hh, m0 + 32 * w);
         }
         for (int kb = 0; kb < nk; kb++) {
             const int s = kb % ns;
@@ -218,8 +235,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-            tc::tma_store_2d(&tmC, wbox, n0, m0 + 32 * warp);
-            tc::tma_store_2d(&tmC, wbox + 4096, n0 + 64, m0 + 32 * warp);
+            if (cstream) {
+                const uint64_t pol = tc::l2_evict_first();
+                tc::tma_store_2d_hint(&tmC, wbox, n0, m0 + 32 * warp, pol);
+                tc::tma_store_2d_hint(&tmC, wbox + 4096, n0 + 64, m0 + 32 * warp, pol);
+            } else {
+                tc::tma_store_2d(&tmC, wbox, n0, m0 + 32 * warp);
+                tc::tma_store_2d(&tmC, wbox + 4096, n0 + 64, m0 + 32 * warp);
+            }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
@@ -495,6 +518,8 @@ int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const vo
         cudaFuncSetAttribute(tc_gemm_persistent_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::PSMEM);
         return v;
     }();
+    // the look-ahead's rest update (max_ctas < 0) streams its C tiles through the L2 (evict first)
+    const int cstream = (max_ctas < 0 && ctma && !env_flag("LYAP_TC_NO_CHINT")) ? 1 : 0;
     KTimer kt(KC_TCGEMM, s, 2.0 * M * N * K, 2.0 * ((double)M * K + (double)N * K + (beta != 0.f ? 2.0 : 1.0) * M * N));
     const int tiles = (int)(grid.x * grid.y);
     // max_ctas < 0: one CTA per tile (SMs come free tile by tile, so a concurrent
@@ -511,10 +536,10 @@ int tc_gemm(cudaStream_t s, int prec, int M, int N, int K, float alpha, const vo
     }
     if (prec == LYAP_BF16)
         tc_gemm_kernel<__nv_bfloat16><<<grid, 128, smem, s>>>(ma, mb, mc, M, N, K, alpha, beta,
-                                                               (__nv_bfloat16 *)C, ldc, colmajor, ctma, ns);
+                                                               (__nv_bfloat16 *)C, ldc, colmajor, ctma, ns, cstream);
     else
         tc_gemm_kernel<__half><<<grid, 128, smem, s>>>(ma, mb, mc, M, N, K, alpha, beta, (__half *)C, ldc,
-                                                       colmajor, ctma, ns);
+                                                       colmajor, ctma, ns, cstream);
     return launched();
 }
 
