@@ -510,7 +510,7 @@ gje_ip_panel_kernel(int n, int k, int K0, int nbk, T *__restrict__ A, T *__restr
         // then lane t writes element t of one row at a time -- 128 contiguous bytes per store
         // instruction (a thread writing its own row touches 32 sectors per instruction: 10 K
         // cycles per panel at n = 16384 against ~4 K this way).
-        if constexpr (NT >= 512) {
+        if constexpr (NT >= 512 || RPT >= 2) {
 #pragma unroll
             for (int h = 0; h < RPT; h++) {
                 const int r = r0 + h;
@@ -825,7 +825,9 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
     LYAP_TRY(launched());
     // threads per CTA: the cluster has at most 16 CTAs; LYAP_GJE_IP_NT overrides (tuning)
     // (measured at n = 16384: 512 threads x 2 rows 2430 cycles per column, 1024 x 1 3440)
-    int nt = n <= 4096 ? 256 : 512, rpt = n <= 8192 ? 1 : 2;
+    // (n = 8192: 256 threads x 2 rows 14.9 ms per inversion, 512 x 1 16.8: the column time follows the
+    // warps per CTA; n = 16384: 512 x 2 40.5 ms, 256 x 4 42.7, 1024 x 1 slower still)
+    int nt = n <= 8192 ? 256 : 512, rpt = n <= 4096 ? 1 : 2;
     if (const char *e = getenv("LYAP_GJE_IP_NT")) nt = atoi(e);
     if (const char *e = getenv("LYAP_GJE_IP_RPT")) rpt = atoi(e);
     if (nt == 128) rpt = 2;
@@ -865,6 +867,7 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
                 if (nt == 128) LYAP_TRY(panel_launch<T, 128, 2, false>(P, n, k, K0, nbk, A, w, xk));
                 else if (nt == 256 && rpt == 1 && fused) LYAP_TRY(panel_launch<T, 256, 1, true>(P, n, k, K0, nbk, A, w, xk));
                 else if (nt == 256 && rpt == 1) LYAP_TRY(panel_launch<T, 256, 1, false>(P, n, k, K0, nbk, A, w, xk));
+                else if (nt == 256 && fused) LYAP_TRY(panel_launch<T, 256, 2, true>(P, n, k, K0, nbk, A, w, xk));
                 else if (nt == 256) LYAP_TRY(panel_launch<T, 256, 2, false>(P, n, k, K0, nbk, A, w, xk));
                 else if (nt == 512 && rpt == 1 && !xout) LYAP_TRY(panel_launch<T, 512, 1, false>(P, n, k, K0, nbk, A, w, xk));
                 else if (nt == 512 && rpt == 1) LYAP_TRY(panel_launch<T, 512, 1, true>(P, n, k, K0, nbk, A, w, xk));
@@ -873,7 +876,7 @@ int gje_ip_invert_t(cudaStream_t s, int n, T *A, T *G, GjeWork &w)
             }
             KTimer kt(KC_GJE_UPDATE, P);
             const bool pdl = n <= 4096 && !env_flag("LYAP_GJE_NO_PDL");
-            const bool xexp = !(nt == 128 || (nt == 256 && rpt == 2) || (nt == 512 && rpt == 1 && !xout));   // panel exported
+            const bool xexp = !(nt == 128 || (nt == 512 && rpt == 1 && !xout));   // panel exported
             if (fused && xexp)
                 LYAP_TRY(rank32_fused_update(P, Prec<T>::code, n, nbk, k, K0, (const float *)w.Pglob, (const float *)w.Tg,
                                              w.invperm, (const T *)w.B + (size_t)K0 * BW, A + K0, n, pdl));
