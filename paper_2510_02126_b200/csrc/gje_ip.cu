@@ -444,6 +444,8 @@ gje_ip_panel_kernel(int n, int k, int K0, int nbk, T *__restrict__ A, T *__restr
             bulk_s2c(mapa(ptx::smem_addr(&PL[j][0]), (uint32_t)lane), ptx::smem_addr(&PLs[j][0]), 128u, mapa(a_mbar + 16u, (uint32_t)lane));
     }
     ptx::mbar_wait(&mbar[2], 0u);
+    // all 32 rows of L11 are here: tell the cluster (the matching wait is at the kernel's end)
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     IPPROF();
 
     // ---- Linv = L11^{-1} (warp 0), Uinv = U11^{-1} (warp 1): column c in the registers of
@@ -618,6 +620,9 @@ gje_ip_panel_kernel(int n, int k, int K0, int nbk, T *__restrict__ A, T *__restr
             for (int e = 0; e < VE; e++) B[(long)(col0 + e) * BW + lane] = from_acc<T>(v[e]);
         }
     }
+    // no CTA leaves while a peer may not yet have received its L11 rows (the copies read this
+    // CTA's staging buffer): every CTA arrived once it held all 32 rows, long ago by now
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 #ifdef LYAP_PANEL_PROF
     IPPROF();
     if (tid == 0 && q == 0 && (k == 0 || k == 544))
